@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the cached generation step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4] [--kernel auto]
+    python bench.py --impl reference ...      # the reference arm (CPU oracle port)
+
+A "step" is one generation step of every stream of the workload (embed ->
+all layers -> head -> selection -> re-embed), i.e. `batch` samples. Default
+workload: BASELINE config 4 (4 blocks x 10 layers, R=128, 2D=256, S=512,
+bf16 weights, fp32 queues, 4,096 streams, Gumbel sampling) -- the config the
+samples/s scaling metric is quoted on. Under torchrun the 4,096 streams are
+split over the ranks (strong scaling, 512/GPU at 8 as BASELINE states); noise
+is keyed by global stream id so the generated sequences do not depend on N.
+
+Prints one JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                  "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        d["source"] = "measured (MEASURED_PEAKS.json)"
+        return d
+    return dict(PEAKS_FALLBACK)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+# ---- clocks sampled during the timed region ------------------------------------------
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active", "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 3:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.05)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        for r in self.rows:
+            try:
+                bits = int(r[2], 16)
+            except ValueError:
+                continue
+            for b, name in REASON_BITS.items():
+                if bits & b:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ---- workload accounting --------------------------------------------------------------
+def step_accounting(cell, batch):
+    """Algorithmic FLOPs and bytes of one step."""
+    wbytes = 2 if cell.weight_dtype == "bf16" else 4
+    flops = 2 * cell.macs_per_sample() * batch
+    weight_bytes = cell.weight_count() * wbytes
+    R, N = cell.residual_channels, cell.total_layers
+    queue_bytes = batch * N * 2 * R * 4  # one slot read + one slot written per layer per stream
+    io_bytes = batch * (R * 4 + 8)  # embedding row + class in/out
+    return flops, weight_bytes + queue_bytes + io_bytes, queue_bytes
+
+
+def traffic_per_step(config_name, kernel):
+    """DRAM bytes per step from the committed ncu --set full summary, if any."""
+    for f in sorted((ROOT / "profiles").glob("ncu_summary_*.json"), reverse=True):
+        try:
+            d = json.loads(f.read_text())
+        except ValueError:
+            continue
+        key = f"{config_name}/{kernel}"
+        if key in d and d[key].get("dram_bytes_per_step"):
+            return d[key]["dram_bytes_per_step"], f.name
+    return None, None
+
+
+# ---- CPU baseline: the oracle port on host cores ------------------------------------
+def cpu_baseline(spec, model, max_seconds=20.0, streams=256):
+    from threadpoolctl import threadpool_info
+
+    from oracle import cell as oc
+
+    threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    o = oc.CellOracle(model, exact=False)
+    B = min(streams, spec.batch)
+    st = oc.CachedCell(o, B)
+    cls = np.full(B, spec.primer_class)
+    streams_ids = np.arange(B)
+    st.step(cls)  # warm-up (allocations, BLAS init)
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        lg = st.step(cls)
+        cls = oc.select(spec.sampler, lg, 2016, streams_ids, st.t)
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= max_seconds or n >= 2000:
+            break
+    return {"value": B * n / el, "unit": "samples/s", "cores": threads, "kind": "port",
+            "sample": f"oracle/cell.py CachedCell fp64 (BLAS), {B} of {spec.batch} streams x "
+                      f"{n} steps of {spec.name}, {el:.1f} s"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--kernel", default="auto", choices=["auto", "simt", "tcgen05"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=0, help="override total streams")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+
+    from paper_1611_09482_b200 import configs
+    from paper_1611_09482_b200.cell import build_cell_model
+
+    spec = configs.by_name(args.config)
+    total_batch = args.batch or spec.batch
+    rank, world, local = dist_env()
+    metric = "generated samples/sec (batch x steps / s)"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        model = build_cell_model(spec.cell)
+        vals = []
+        cb = None
+        for _ in range(max(1, min(args.steps, 3))):
+            cb = cpu_baseline(spec, model, max_seconds=args.cpu_seconds / 2)
+            vals.append(cb["value"])
+        v = statistics.median(vals)
+        cb["value"] = v
+        line = {"impl": "reference", "metric": metric, "value": v, "unit": "samples/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1e3 * total_batch / v, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded weights, primer class 128, counter-hash Gumbel noise)",
+                "config": {"workload": spec.name, "streams": total_batch,
+                           "note": "reference arm = CPU oracle port (the reference is pure "
+                                   "Python/numba and has no cell; see DESIGN.md)"},
+                "cpu_baseline": cb,
+                "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                        "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local if world > 1 else 0)
+    torch.cuda.set_device(dev)
+
+    from paper_1611_09482_b200 import CellGenerator, Sampler
+
+    if total_batch % world:
+        raise SystemExit("batch must divide over the ranks")
+    B = total_batch // world
+    offset = rank * B
+    model = build_cell_model(spec.cell)
+    gen = CellGenerator(model, B, kernel=args.kernel)
+    sampler = Sampler(spec.sampler, configs.NOISE_SEED, offset)
+    primer = torch.full((1, B), spec.primer_class, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    # warm-up
+    out_w, _ = gen.generate(primer, args.warmup, sampler)
+    torch.cuda.synchronize()
+
+    # device-timed K steps, inputs resident in HBM
+    gen.reset()
+    out = torch.empty((args.steps, B), dtype=torch.int32, device=dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev.index) as clk:
+        e0.record(stream)
+        gen.generate(primer, args.steps, sampler, out=out)
+        e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1)
+    launches = gen.last_launch_count
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # end-to-end through the public host-buffer API (copies inside the timed region)
+    gen.reset()
+    host_in = np.full((1, B), spec.primer_class, dtype=np.int32)
+    host_out = np.empty((args.steps, B), dtype=np.int32)
+    gen.generate_host(host_in, 1, sampler, out=host_out[:1])  # warm the host path
+    gen.reset()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    gen.generate_host(host_in, args.steps, sampler, out=host_out)
+    e2e_s = time.perf_counter() - t0
+    barrier()
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    same = bool(np.array_equal(host_out, out.cpu().numpy()))
+
+    # final gather of the generated sequences (the only collective)
+    gather_ms = None
+    if world > 1:
+        g0 = time.perf_counter()
+        full = torch.empty((world, args.steps, B), dtype=torch.int32, device=dev)
+        torch.distributed.all_gather_into_tensor(full, out)
+        torch.cuda.synchronize()
+        gather_ms = 1e3 * (time.perf_counter() - g0)
+
+    if rank == 0:
+        peaks = load_peaks()
+        flops, bytes_step, qbytes = step_accounting(spec.cell, total_batch)
+        per_gpu_flops, per_gpu_bytes, _ = step_accounting(spec.cell, B)
+        s_per_step = ms / 1e3 / args.steps
+        value = total_batch * args.steps / (ms / 1e3)
+        tensor_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * 1e12
+        hbm = peaks["hbm_gbs"] * 1e9
+        fp32_peak = 148 * 128 * 2 * 1.965e9  # not measured; computed at max boost
+        comp_peak = tensor_peak if spec.cell.weight_dtype == "bf16" else fp32_peak
+        t_flop = per_gpu_flops / comp_peak
+        t_byte = per_gpu_bytes / hbm
+        kname = gen.kernel
+        traffic, tsrc = traffic_per_step(spec.name, kname)
+        if t_flop >= t_byte:
+            roof = {"bound": "tensor" if spec.cell.weight_dtype == "bf16" else "fp32",
+                    "achieved": per_gpu_flops / s_per_step / 1e12, "peak": comp_peak / 1e12,
+                    "unit": "TFLOP/s"}
+        else:
+            roof = {"bound": "hbm", "achieved": per_gpu_bytes / s_per_step / 1e9,
+                    "peak": hbm / 1e9, "unit": "GB/s"}
+        roof["frac"] = roof["achieved"] / roof["peak"]
+        roof["traffic"] = traffic * args.steps if traffic else None
+        roof["traffic_unit"] = "bytes per launch (K steps)"
+        roof["step_roofline_us"] = 1e6 * max(t_flop, t_byte)
+        roof["step_roofline_frac"] = max(t_flop, t_byte) / s_per_step
+        roof["kernel"] = f"cell_{kname} (one persistent launch per generate call)"
+        roof["peak_source"] = peaks["source"] + (
+            ", bf16 sustained" if spec.cell.weight_dtype == "bf16" else ", fp32 = 148x128x2x1.965GHz (computed)")
+        if tsrc:
+            roof["traffic_source"] = f"profiles/{tsrc}"
+        line = {
+            "metric": metric, "value": value, "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "bf16" if spec.cell.weight_dtype == "bf16" else "f32",
+            "data": "synthetic (seeded N(0,1/fan_in) weights, primer class 128, "
+                    "counter-hash Gumbel noise)",
+            "config": {"workload": spec.name, "streams": total_batch, "streams_per_gpu": B,
+                       "layers": spec.cell.total_layers, "residual": spec.cell.residual_channels,
+                       "skip": spec.cell.skip_channels, "kernel": kname,
+                       "parallelism": f"streams sharded x{world}",
+                       "l2": "queues 8.6 GB >> L2; each step touches "
+                             f"{qbytes / 1e6:.0f} MB of fresh queue slots (no flush needed)"},
+            "roofline": roof,
+            "e2e": {"value": total_batch * args.steps / e2e_s, "unit": "samples/s",
+                    "h2d_bytes_per_step": B * 4 / args.steps, "d2h_bytes_per_step": B * 4,
+                    "api": "CellGenerator.generate_host -> fw_cell_generate_host",
+                    "matches_device_run": same},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+        }
+        if gather_ms is not None:
+            line["gather_ms"] = gather_ms
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(spec, model, max_seconds=args.cpu_seconds)
+        print(json.dumps(line), flush=True)
+    gen.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,293 @@
+// K1: persistent fp32 CUDA-core step kernel for the gated cell.
+//
+// One CTA owns a tile of BT streams for the whole generate call and loops on
+// the device over steps and layers (no launch per step or per layer; SURVEY
+// section 3 "Host<->device crossings"). Per layer it performs the reference's
+// pop -> compute -> push cycle (fast.py:131-213) for its streams:
+//   pop/push : one HBM slot (t mod d_l) of the layer's ring queue is read
+//              (x_l[t-d]) and overwritten with the layer input x_l[t] by the
+//              same thread, so read-before-write needs no barrier;
+//   compute  : a = W0 x_l[t] + W1 x_l[t-d] + b, z = tanh(a[:D]) * sigmoid(a[D:]),
+//              s += W_skip z + b_skip, x_{l+1} = x_l + W_res z + b_res;
+// then the ReLU-1x1-ReLU-1x1 head, the selection rule and the re-embedding.
+// Activations stay in shared memory; weights (fp32, transposed to [in][out]
+// for coalescing) stream from L2, each weight load reused BT times.
+// Narrow layers split K across thread groups and reduce through smem so a
+// batch-1 stream still uses all 256 threads.
+//
+// This kernel serves every configuration (fp32 cfg1/2/3/5 and, with
+// bf16-rounded weights and fp32 math, cfg4); the tcgen05 kernel (cell_tc.cu)
+// replaces it for large batches.
+#include "internal.h"
+
+namespace fw {
+namespace {
+
+constexpr int NT = 256;
+
+struct SimtParams {
+  CellDims d;
+  int B;
+  const int* dil;
+  const int64_t* qoff;
+  float* queue;
+  SimtWeights w;
+  CellRun run;
+};
+
+// out[b][o] = epi(b, o, sum_c WT[c][o] * in[b][c]) for o < N, b < BT.
+template <int BT, typename Epi>
+__device__ __forceinline__ void gemv(const float* __restrict__ WT, int K, int N,
+                                     const float* in, int ldin, float* red, Epi epi) {
+  const int tid = threadIdx.x;
+  if (N >= NT / 2) {
+    for (int o = tid; o < N; o += NT) {
+      float acc[BT];
+#pragma unroll
+      for (int b = 0; b < BT; ++b) acc[b] = 0.f;
+      int c = 0;
+      for (; c + 4 <= K; c += 4) {
+        float w0 = __ldg(WT + (size_t)(c + 0) * N + o);
+        float w1 = __ldg(WT + (size_t)(c + 1) * N + o);
+        float w2 = __ldg(WT + (size_t)(c + 2) * N + o);
+        float w3 = __ldg(WT + (size_t)(c + 3) * N + o);
+#pragma unroll
+        for (int b = 0; b < BT; ++b) {
+          const float* x = in + b * ldin + c;
+          acc[b] = fmaf(w0, x[0], acc[b]);
+          acc[b] = fmaf(w1, x[1], acc[b]);
+          acc[b] = fmaf(w2, x[2], acc[b]);
+          acc[b] = fmaf(w3, x[3], acc[b]);
+        }
+      }
+      for (; c < K; ++c) {
+        float w0 = __ldg(WT + (size_t)c * N + o);
+#pragma unroll
+        for (int b = 0; b < BT; ++b) acc[b] = fmaf(w0, in[b * ldin + c], acc[b]);
+      }
+#pragma unroll
+      for (int b = 0; b < BT; ++b) epi(b, o, acc[b]);
+    }
+    return;
+  }
+  // Split K over G groups of N threads, reduce partials in a fixed order.
+  const int G = NT / N;
+  const int o = tid % N, g = tid / N;
+  const int kc = (K + G - 1) / G;
+  const int k0 = g * kc, k1 = min(K, k0 + kc);
+  float acc[BT];
+#pragma unroll
+  for (int b = 0; b < BT; ++b) acc[b] = 0.f;
+  if (g < G) {
+    for (int c = k0; c < k1; ++c) {
+      float w0 = __ldg(WT + (size_t)c * N + o);
+#pragma unroll
+      for (int b = 0; b < BT; ++b) acc[b] = fmaf(w0, in[b * ldin + c], acc[b]);
+    }
+#pragma unroll
+    for (int b = 0; b < BT; ++b) red[(g * BT + b) * N + o] = acc[b];
+  }
+  __syncthreads();
+  for (int e = tid; e < BT * N; e += NT) {
+    const int b = e / N, oo = e % N;
+    float v = 0.f;
+    for (int gg = 0; gg < G; ++gg) v += red[(gg * BT + b) * N + oo];
+    epi(b, oo, v);
+  }
+}
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
+
+// Warp-wide (value, index) maximum; ties go to the lower index (numpy argmax).
+__device__ __forceinline__ void warp_argmax(float& v, int& i) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    float ov = __shfl_xor_sync(0xffffffffu, v, off);
+    int oi = __shfl_xor_sync(0xffffffffu, i, off);
+    if (ov > v || (ov == v && oi < i)) {
+      v = ov;
+      i = oi;
+    }
+  }
+}
+
+// Selection for one stream by one warp over A logits in smem.
+__device__ int select_class(const float* lg, int A, int mode, uint32_t prefix) {
+  const int lane = threadIdx.x & 31;
+  if (mode == FW_SAMPLE_INVCDF) {
+    float m = -INFINITY;
+    for (int a = lane; a < A; a += 32) m = fmaxf(m, lg[a]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    // contiguous chunk per lane, sequential inside, scan across lanes
+    const int chunk = (A + 31) / 32;
+    const int a0 = min(A, lane * chunk), a1 = min(A, a0 + chunk);
+    float part = 0.f;
+    for (int a = a0; a < a1; ++a) part += expf(lg[a] - m);
+    float incl = part;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      float o = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += o;
+    }
+    const float total = __shfl_sync(0xffffffffu, incl, 31);
+    const float thr = noise_uniform(prefix, kUniformClass) * total;
+    float run = incl - part;
+    int found = A;
+    for (int a = a0; a < a1; ++a) {
+      run += expf(lg[a] - m);
+      if (run > thr) {
+        found = a;
+        break;
+      }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, off));
+    return found < A ? found : A - 1;
+  }
+  float best = -INFINITY;
+  int bi = A;
+  for (int a = lane; a < A; a += 32) {
+    float v = lg[a];
+    if (mode == FW_SAMPLE_GUMBEL) v += -logf(-logf(noise_uniform(prefix, (uint32_t)a)));
+    if (v > best) {
+      best = v;
+      bi = a;
+    }
+  }
+  warp_argmax(best, bi);
+  return bi;
+}
+
+template <int BT>
+__global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
+  extern __shared__ float smem[];
+  const CellDims d = p.d;
+  const int R = d.R, D = d.D, S = d.S, H = d.H, A = d.A, L = d.L;
+  float* xx = smem;                 // [BT][2R]: x_l[t] | x_l[t-d]
+  float* a = xx + BT * 2 * R;       // [BT][2D]
+  float* z = a + BT * 2 * D;        // [BT][D]
+  float* s = z + BT * D;            // [BT][S]
+  float* hb = s + BT * S;           // [BT][H]
+  float* lg = hb + BT * H;          // [BT][A]
+  float* red = lg + BT * A;         // [NT * BT] K-split partials
+  int* cls = reinterpret_cast<int*>(red + NT * BT);  // [BT]
+
+  const int tid = threadIdx.x;
+  const int s0 = blockIdx.x * BT;
+  const int nb = min(BT, p.B - s0);
+  const CellRun& run = p.run;
+  const int B = p.B;
+
+  if (tid < BT) cls[tid] = (tid < nb) ? run.inputs[s0 + tid] : 0;
+  __syncthreads();
+
+  for (int i = 0; i < run.n_steps; ++i) {
+    const int64_t t = run.t0 + i;
+    // x_0 = E[c_t]; s = 0
+    for (int e = tid; e < BT * R; e += NT) {
+      const int b = e / R, r = e % R;
+      xx[b * 2 * R + r] = __ldg(p.w.embed + (size_t)cls[b] * R + r);
+    }
+    for (int e = tid; e < BT * S; e += NT) s[e] = 0.f;
+    __syncthreads();
+
+    for (int l = 0; l < L; ++l) {
+      // pop + push on slot t mod d_l: read x_l[t-d], cache x_l[t] (fast.py:192)
+      const int dl = p.dil[l];
+      float* q = p.queue + p.qoff[l] + (size_t)(t % dl) * B * R + (size_t)s0 * R;
+      for (int e = tid; e < nb * R; e += NT) {
+        const int b = e / R, r = e % R;
+        const float old = q[e];
+        q[e] = xx[b * 2 * R + r];
+        xx[b * 2 * R + R + r] = old;
+      }
+      __syncthreads();
+      const float* db = p.w.dil_b + (size_t)l * 2 * D;
+      gemv<BT>(p.w.dilT + (size_t)l * 2 * R * 2 * D, 2 * R, 2 * D, xx, 2 * R, red,
+               [&](int b, int o, float v) { a[b * 2 * D + o] = v + db[o]; });
+      __syncthreads();
+      for (int e = tid; e < BT * D; e += NT) {
+        const int b = e / D, j = e % D;
+        z[e] = tanhf(a[b * 2 * D + j]) * sigmoidf_(a[b * 2 * D + D + j]);
+      }
+      __syncthreads();
+      const float* sb = p.w.skip_b + (size_t)l * S;
+      gemv<BT>(p.w.skipT + (size_t)l * D * S, D, S, z, D, red,
+               [&](int b, int o, float v) { s[b * S + o] += v + sb[o]; });
+      if (l + 1 < L) {
+        __syncthreads();
+        const float* rb = p.w.res_b + (size_t)l * R;
+        gemv<BT>(p.w.resT + (size_t)l * D * R, D, R, z, D, red,
+                 [&](int b, int o, float v) { xx[b * 2 * R + o] += v + rb[o]; });
+      }
+      __syncthreads();
+    }
+    // head: logits = W2 relu(W1 relu(s) + b1) + b2
+    for (int e = tid; e < BT * S; e += NT) s[e] = fmaxf(s[e], 0.f);
+    __syncthreads();
+    gemv<BT>(p.w.h1T, S, H, s, S, red,
+             [&](int b, int o, float v) { hb[b * H + o] = fmaxf(v + p.w.h1_b[o], 0.f); });
+    __syncthreads();
+    gemv<BT>(p.w.h2T, H, A, hb, H, red,
+             [&](int b, int o, float v) { lg[b * A + o] = v + p.w.h2_b[o]; });
+    __syncthreads();
+
+    if (run.logits != nullptr && i < run.n_logit_steps) {
+      float* dst = run.logits + ((size_t)i * B + s0) * A;
+      for (int e = tid; e < nb * A; e += NT) dst[e] = lg[e];
+    }
+    const int warp = tid >> 5;
+    for (int b = warp; b < nb; b += NT / 32) {
+      const uint32_t gs = (uint32_t)(run.stream_offset + s0 + b);
+      const uint32_t prefix = noise_prefix(run.seed, gs, (uint32_t)t);
+      const int c = select_class(lg + b * A, A, run.mode, prefix);
+      if ((tid & 31) == 0) {
+        run.out[(size_t)i * B + s0 + b] = c;
+        cls[b] = (i + 1 < run.n_inputs) ? run.inputs[(size_t)(i + 1) * B + s0 + b] : c;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <int BT>
+size_t smem_bytes(const CellDims& d) {
+  return sizeof(float) * (size_t)(BT * (2 * d.R + 2 * d.D + d.D + d.S + d.H + d.A) + NT * BT) +
+         sizeof(int) * BT;
+}
+
+template <int BT>
+cudaError_t launch_bt(const SimtParams& p, cudaStream_t st) {
+  const size_t sm = smem_bytes<BT>(p.d);
+  cudaError_t e = cudaFuncSetAttribute(cell_simt_kernel<BT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  const int grid = (p.B + BT - 1) / BT;
+  cell_simt_kernel<BT><<<grid, NT, sm, st>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_cell_simt(const Handle& h, const CellRun& run, cudaStream_t st,
+                             int64_t* launches) {
+  SimtParams p;
+  p.d = h.dims;
+  p.B = h.batch;
+  p.dil = h.d_dil;
+  p.qoff = h.d_qoff;
+  p.queue = h.d_queue;
+  p.w = h.w;
+  p.run = run;
+  *launches = 1;
+  // Streams per CTA: enough CTAs to cover the SMs, up to 8 streams sharing
+  // each weight load.
+  const int B = h.batch;
+  if (B >= 148 * 8) return launch_bt<8>(p, st);
+  if (B >= 148 * 4) return launch_bt<4>(p, st);
+  if (B >= 148 * 2) return launch_bt<2>(p, st);
+  return launch_bt<1>(p, st);
+}
+
+}  // namespace fw

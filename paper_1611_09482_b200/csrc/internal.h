@@ -1,0 +1,147 @@
+// Internal definitions shared by the C-ABI (capi.cu) and the kernel files.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/fastwavenet.h"
+
+namespace fw {
+
+// Last-error slot (thread-local), set by every failing entry point.
+void set_error(const std::string& msg);
+
+// ---- noise hash (bit-identical to oracle/noise.py) -------------------------
+__host__ __device__ __forceinline__ uint32_t mix32(uint32_t x) {
+  x ^= x >> 16;
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  x ^= x >> 16;
+  return x;
+}
+constexpr uint32_t kSeedSalt = 0x243F6A88u;
+constexpr uint32_t kUniformClass = 0xFFFFFFFFu;
+
+// Hash prefix of (seed, stream, step); the class is mixed in last.
+__host__ __device__ __forceinline__ uint32_t noise_prefix(uint32_t seed, uint32_t stream,
+                                                          uint32_t step) {
+  uint32_t h = mix32(seed ^ kSeedSalt);
+  h = mix32(h ^ stream);
+  return mix32(h ^ step);
+}
+// u in (0,1): ((h >> 8) + 0.5) * 2^-24 -- exact in fp32.
+__host__ __device__ __forceinline__ float noise_uniform(uint32_t prefix, uint32_t cls) {
+  uint32_t h = mix32(prefix ^ cls);
+  return (static_cast<float>(h >> 8) + 0.5f) * (1.0f / 16777216.0f);
+}
+
+// ---- cell problem description ------------------------------------------------
+struct CellDims {
+  int L, R, D, S, H, A;
+  int dtype;  // FW_DTYPE_*
+};
+
+// Arguments of one generate call (device pointers), shared by all cell kernels.
+struct CellRun {
+  const int32_t* inputs;  // [n_inputs][B]
+  int32_t n_inputs;
+  int32_t n_steps;
+  int32_t* out;           // [n_steps][B]
+  float* logits;          // [n_logit_steps][B][A] or null
+  int32_t n_logit_steps;
+  int64_t t0;             // absolute step index of the first step
+  int32_t mode;           // FW_SAMPLE_*
+  uint32_t seed;
+  int64_t stream_offset;
+};
+
+// fp32 SIMT weights: every matrix transposed to [in][out] so a warp's
+// consecutive output channels read consecutive addresses.
+struct SimtWeights {
+  float* embed;  // [A][R]
+  float* dilT;   // [L][2R][2D]  rows 0..R-1 tap 0 (current), R..2R-1 tap 1 (d back)
+  float* dil_b;  // [L][2D]
+  float* resT;   // [L][D][R]
+  float* res_b;  // [L][R]
+  float* skipT;  // [L][D][S]
+  float* skip_b; // [L][S]
+  float* h1T;    // [S][H]
+  float* h1_b;   // [H]
+  float* h2T;    // [H][A]
+  float* h2_b;   // [A]
+};
+
+// tcgen05 path device state (see cell_tc.cu).
+struct TcState;
+
+struct Handle;
+
+// Launchers (return cudaError_t of the launch); defined in the kernel files.
+cudaError_t launch_cell_simt(const Handle& h, const CellRun& run, cudaStream_t st,
+                             int64_t* launches);
+cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64_t* launches);
+bool tc_supported(const CellDims& d, int batch, std::string* why);
+int tc_create(Handle& h, const fw_cell_desc* desc);
+void tc_destroy(Handle& h);
+
+struct PlainDev {
+  int n_layers, w, act;
+  int* dil;         // [n]
+  int* cin;         // [n]
+  int* cout;        // [n]
+  int64_t* woff;    // [n] offset into taps
+  int64_t* boff;    // [n] offset into bias
+  int64_t* qoff;    // [n] offset into queue (doubles)
+  int64_t* roff;    // [n] offset of the layer's rows in the rec buffer
+  int64_t* soff;    // [n] offset of the layer's rows in the states buffer
+  double* taps;
+  double* bias;
+  double* queue;
+  int cmax;
+  int64_t rec_rows, state_rows;
+};
+
+cudaError_t launch_plain_generate(const Handle& h, const double* inputs, int n_inputs,
+                                  int n_steps, double* out, cudaStream_t st);
+cudaError_t launch_plain_pop(const Handle& h, double* rec, cudaStream_t st);
+cudaError_t launch_plain_compute(const Handle& h, const double* in, const double* rec,
+                                 double* out, double* states, cudaStream_t st);
+cudaError_t launch_plain_push(const Handle& h, const double* states, cudaStream_t st);
+
+struct Handle {
+  int is_plain = 0;
+  int device = 0;
+  int kernel = FW_KERNEL_SIMT;
+  int32_t batch = 0;
+  int64_t t = 0;
+  int64_t last_launches = 0;
+  int popped = 0;
+
+  // cell
+  CellDims dims{};
+  std::vector<int> dil;
+  int* d_dil = nullptr;
+  int64_t* d_qoff = nullptr;
+  float* d_queue = nullptr;
+  int64_t queue_elems = 0;
+  SimtWeights w{};
+  TcState* tc = nullptr;
+
+  // plain
+  PlainDev p{};
+  std::vector<int> pdil, pcin;
+
+  // scratch for the *_host entry points
+  int32_t* d_io = nullptr;
+  int64_t d_io_elems = 0;
+};
+
+}  // namespace fw
+
+struct fw_handle {
+  fw::Handle h;
+};

@@ -1,0 +1,114 @@
+"""GPU plain mode (fp64 kernel) against the reference's own outputs.
+
+Golden outputs come from the unmodified reference (tests/golden/
+plain_reference.npz). Linear stacks must match bit-exactly (same pinned
+order, no FMA); tanh stacks differ from glibc's tanh only in the last ulp of
+CUDA's double tanh, so they are held to 1e-12 relative, the reference's own
+documented fallback tolerance.
+"""
+
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+from paper_1611_09482_b200 import (
+    QueueStateError, compute_step, fast_generate, fast_step, init_state, pop_phase, push_phase)
+from paper_1611_09482_b200.model import LayerWeights, Model, ModelConfig, build_model
+
+pytestmark = pytest.mark.gpu
+
+G = np.load(Path(__file__).parent / "golden" / "plain_reference.npz")
+NAMES = sorted({k.split("/")[0] for k in G.files if not k.startswith("delay")})
+
+
+def model_of(name):
+    c = G[f"{name}/config"]
+    return build_model(ModelConfig(int(c[0]), int(c[1]), int(c[2]), int(c[3]), int(c[4]),
+                                   "tanh" if c[5] else "linear", int(c[6])))
+
+
+def assert_match(got, want, tanh):
+    if tanh:
+        np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-300)
+    else:
+        assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("name", NAMES)
+def test_teacher_forced_and_free_run_match_reference(cuda, name):
+    m = model_of(name)
+    tanh = m.config.activation == "tanh"
+    xs = G[f"{name}/xs"]
+    st = init_state(m)
+    got = np.array([fast_step(st, float(x), m) for x in xs])
+    assert_match(got, G[f"{name}/tf"], tanh)
+    assert st.step_index == len(xs)
+    free = G[f"{name}/free"]
+    out = fast_generate(m, G[f"{name}/primer"], len(free))
+    assert out.start_index == len(G[f"{name}/primer"])
+    assert_match(out.scalars(), free, tanh)
+
+
+@pytest.mark.parametrize("layers", [1, 3, 4])
+def test_delay_line_exact(cuda, layers):
+    cfg = ModelConfig(1, layers, 2, 2, 1, "linear", 0)
+    lws = []
+    for l in range(layers):
+        taps = np.zeros((2, 1, 1))
+        taps[1 if l == layers - 1 else 0, 0, 0] = 1.0
+        lws.append(LayerWeights(taps, np.zeros(1)))
+    m = Model(cfg, tuple(lws))
+    xs = G[f"delay{layers}/xs"]
+    st = init_state(m)
+    got = np.array([fast_step(st, float(x), m) for x in xs])
+    assert np.array_equal(got, G[f"delay{layers}/tf"])
+
+
+def test_batched_streams_are_independent(cuda):
+    m = model_of("grid100")
+    xs = np.random.default_rng(3).uniform(-1, 1, (12, 5))
+    st = init_state(m, batch=5)
+    got = np.stack([fast_step(st, x, m) for x in xs])
+    for b in range(5):
+        st1 = init_state(m)
+        one = np.array([fast_step(st1, float(x), m) for x in xs[:, b]])
+        assert np.array_equal(got[:, b], one)
+
+
+def test_phase_api_and_errors(cuda):
+    m = build_model(ModelConfig(1, 4, hidden_channels=1, activation="tanh", init_seed=7))
+    st = init_state(m)
+    assert [q.capacity for q in st.queues] == [1, 2, 4, 8]
+    assert st.cached_scalar_count() == 15
+    rec = pop_phase(st)
+    assert len(rec.per_layer) == 4 and all(np.array_equal(r[0], np.zeros(1)) for r in rec.per_layer)
+    with pytest.raises(QueueStateError):
+        pop_phase(st)
+    y, new_states, macs = compute_step(m, 0.3, rec)
+    assert macs.multiply_accumulates == 8 and macs.node_evaluations == 4
+    push_phase(st, new_states)
+    assert st.step_index == 1
+    with pytest.raises(QueueStateError):
+        push_phase(st, new_states)
+    # the pushed value is the layer input: the next pop of layer 0 at t=1 reads t-1 = 0.3
+    st2 = init_state(m)
+    y_ref = fast_step(st2, 0.3, m)
+    assert y == y_ref or abs(y - y_ref) < 1e-15
+    rec2 = pop_phase(st)
+    assert rec2.per_layer[0][0][0] == 0.3
+    assert np.array_equal(rec2.per_layer[1][0], np.zeros(1))  # layer 1 has d=2
+
+
+def test_foreign_state_rejected(cuda):
+    m = model_of("grid000")
+    other = build_model(ModelConfig(blocks=2, layers_per_block=2, init_seed=1))
+    with pytest.raises(ValueError, match="architecture"):
+        fast_step(init_state(other), 0.0, m)
+
+
+def test_generate_zero_steps_is_empty(cuda):
+    m = model_of("grid000")
+    assert len(fast_generate(m, [0.5], 0)) == 0
+    with pytest.raises(ValueError):
+        fast_generate(m, [0.5], -1)
