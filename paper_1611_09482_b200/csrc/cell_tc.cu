@@ -1,13 +1,698 @@
-// K2 placeholder: tcgen05 path not built yet.
+// K2: bf16 tcgen05 step kernels for large batches (BASELINE config 4).
+//
+// One generation step of B streams = four launches on the caller's stream:
+//
+//  1. chain  (B/128 CTAs, 320 threads): per 128-stream tile, the 40-layer
+//     dependent chain. Per layer: pop/push of the HBM ring slot (fp32, 16-byte
+//     accesses), x_t | x_{t-d} -> bf16 swizzled operand in smem, one
+//     tcgen05 MMA group [128 x 256] += [128 x 256] . [256 x 256]^T into TMEM,
+//     the tanh*sigmoid gate in the TMEM->register epilogue, z -> smem operand
+//     (+ a z stash in HBM), then the residual MMA [128 x 128] += z . W_res^T
+//     accumulating straight onto x, which lives in TMEM for the whole step.
+//     Weights stream through a 4-stage ring of 32 KB bulk copies (UBLKCP)
+//     issued by a producer warp; one elected thread issues the MMAs.
+//  2. skip   GEMM  s = [z_0 .. z_{L-1}] . W_skip_cat^T + sum_l b_skip_l, ReLU
+//     (K = L*D = 5120): the skip sum of every layer done as ONE big-K GEMM on
+//     (B/128) x (S/128) CTAs instead of S more TMEM columns per layer.
+//  3. head1  GEMM  h = ReLU(s . W1^T + b1)
+//  4. head2  GEMM  logits = h . W2^T + b2, fused selection (argmax / inverse
+//     CDF / Gumbel-max with the counter hash) and teacher/feedback of the next
+//     input class.
+//
+// Numerics: bf16 operands, fp32 accumulation, fp32 residual stream (TMEM) and
+// fp32 queues, as BASELINE config 4 specifies; tanh via tanh.approx.f32.
+#include <cuda_bf16.h>
+
+#include <cstring>
+#include <vector>
+
 #include "internal.h"
+#include "tc_ptx.cuh"
+
 namespace fw {
-bool tc_supported(const CellDims&, int, std::string* why) {
-  if (why) *why = "not built";
-  return false;
+
+struct TcState {
+  int ntile = 0;
+  uint8_t* wchain = nullptr;  // per layer: 4 dil chunks [256][64] + 2 res chunks [128][64]
+  uint8_t* wskip = nullptr;   // [S/128][L*D/64] chunks of [128][64]
+  uint8_t* wh1 = nullptr;     // [H/128][S/64] chunks of [128][64]
+  uint8_t* wh2 = nullptr;     // [H/64] chunks of [A=256][64]
+  float* skip_bsum = nullptr;  // [S]
+  uint8_t* zimg = nullptr;    // [ntile][L*D/64][16 KB]
+  uint8_t* simg = nullptr;    // [ntile][S/64][16 KB]
+  uint8_t* himg = nullptr;    // [ntile][H/64][16 KB]
+  int32_t* cls = nullptr;     // [B]
+};
+
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
+constexpr int kChainStages = 4;
+constexpr uint32_t kChainStage = 32768;
+constexpr uint32_t kDilChunk = 32768;   // [256 rows][64] bf16
+constexpr uint32_t kResChunk = 16384;   // [128 rows][64] bf16
+constexpr uint32_t kLayerBytes = 4 * kDilChunk + 2 * kResChunk;
+constexpr uint32_t kTile = 16384;       // [128 rows][64] bf16 activation chunk
+constexpr int kR = 128, kD = 128;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
-int tc_create(Handle&, const fw_cell_desc*) { return FW_ERR_UNSUPPORTED; }
-void tc_destroy(Handle&) {}
-cudaError_t launch_cell_tc(Handle&, const CellRun&, cudaStream_t, int64_t*) {
-  return cudaErrorNotSupported;
+
+struct ChainArgs {
+  int B, L;
+  int64_t t;
+  const int* dil;
+  const int64_t* qoff;
+  float* queue;
+  const uint8_t* w;
+  const float* embed;  // [A][128]
+  const float* dil_b;  // [L][256]
+  const float* res_b;  // [L][128]
+  const int32_t* cls;  // [B]
+  uint8_t* zimg;
+};
+
+__device__ __forceinline__ void ld64(float (&v)[64], const float* p) {
+  const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float4 f = q[i];
+    v[4 * i] = f.x;
+    v[4 * i + 1] = f.y;
+    v[4 * i + 2] = f.z;
+    v[4 * i + 3] = f.w;
+  }
 }
+__device__ __forceinline__ void st64(float* p, const float (&v)[64]) {
+  float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) q[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+}
+// 64 fp32 -> one 128-byte bf16 row of a swizzled [128][64] image
+__device__ __forceinline__ void row_to_image(uint32_t img_saddr, int r, const float (&v)[64]) {
+#pragma unroll
+  for (int p = 0; p < 8; ++p)
+    st_shared_v4(img_saddr + swz(r, p), pack_bf16(v[8 * p], v[8 * p + 1]),
+                 pack_bf16(v[8 * p + 2], v[8 * p + 3]), pack_bf16(v[8 * p + 4], v[8 * p + 5]),
+                 pack_bf16(v[8 * p + 6], v[8 * p + 7]));
+}
+
+__global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* X = smem;                  // 4 chunks: x_t[0:64], x_t[64:128], x_{t-d}[0:64], x_{t-d}[64:128]
+  uint8_t* Z = smem + 4 * kTile;      // 2 chunks
+  uint8_t* ring = smem + 6 * kTile;   // kChainStages x 32 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kChainStages * kChainStage);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + kChainStages;
+  uint64_t* a_ready = bars + 2 * kChainStages;
+  uint64_t* z_ready = a_ready + 1;
+  uint64_t* acc_full = a_ready + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(a_ready + 3);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x;
+  const int L = a.L;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kChainStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(a_ready, 256);
+    mbar_init(z_ready, 256);
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- weight producer ----
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int l = 0; l < L; ++l) {
+        const uint8_t* wl = a.w + (size_t)l * kLayerBytes;
+        const int nchunk = (l + 1 < L) ? 6 : 4;
+        for (int c = 0; c < nchunk; ++c) {
+          const uint32_t bytes = c < 4 ? kDilChunk : kResChunk;
+          const uint8_t* src = c < 4 ? wl + c * kDilChunk : wl + 4 * kDilChunk + (c - 4) * kResChunk;
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&full[stage], bytes);
+          bulk_g2s(ring + stage * kChainStage, src, bytes, &full[stage]);
+          if (++stage == kChainStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer ----
+      int stage = 0;
+      uint32_t phase = 0, a_par = 0, z_par = 0;
+      const uint32_t id_dil = idesc_bf16(128, 256), id_res = idesc_bf16(128, 128);
+      const uint32_t xs = smem_u32(X), zs = smem_u32(Z), rs = smem_u32(ring);
+      for (int l = 0; l < L; ++l) {
+        mbar_wait(a_ready, a_par);
+        a_par ^= 1;
+        tc_fence_after();
+        for (int c = 0; c < 4; ++c) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16(tmem, sdesc_sw128(xs + c * kTile + kk * 32),
+                     sdesc_sw128(rs + stage * kChainStage + kk * 32), id_dil, (c | kk) != 0);
+          mma_commit(&empty[stage]);
+          if (++stage == kChainStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(acc_full);
+        if (l + 1 < L) {
+          mbar_wait(z_ready, z_par);
+          z_par ^= 1;
+          tc_fence_after();
+          for (int c = 0; c < 2; ++c) {
+            mbar_wait(&full[stage], phase);
+            tc_fence_after();
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16(tmem + 256, sdesc_sw128(zs + c * kTile + kk * 32),
+                       sdesc_sw128(rs + stage * kChainStage + kk * 32), id_res, 1);
+            mma_commit(&empty[stage]);
+            if (++stage == kChainStages) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          mma_commit(acc_full);
+        }
+      }
+    }
+    __syncwarp();
+  } else {  // ---- epilogue warps 2..9 ----
+    const int sub = warp & 3, h = (warp - 2) >> 2;
+    const int r = sub * 32 + lane;
+    const int stream = tile * 128 + r;
+    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
+    const uint32_t xs = smem_u32(X), zs = smem_u32(Z);
+    const int c = a.cls[stream];
+    uint32_t acc_par = 0;
+    float q[64];
+    auto qptr = [&](int l) {
+      return a.queue + a.qoff[l] + (size_t)(a.t % a.dil[l]) * a.B * kR + (size_t)stream * kR + 64 * h;
+    };
+    float* qp = qptr(0);
+    ld64(q, qp);
+    uint8_t* zdst = a.zimg + (size_t)tile * (L * 2) * kTile;
+    for (int l = 0; l < L; ++l) {
+      // ---- pop/push + operand build ----
+      float x[64];
+      if (l == 0) {
+        ld64(x, a.embed + (size_t)c * kR + 64 * h);
+      } else {
+        mbar_wait(acc_full, acc_par);
+        acc_par ^= 1;
+        tc_fence_after();
+        tmem_ld32(trow + 256 + 64 * h, *reinterpret_cast<float(*)[32]>(x));
+        tmem_ld32(trow + 256 + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
+        tmem_wait_ld();
+        const float* rb = a.res_b + (size_t)(l - 1) * kR + 64 * h;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) x[i] += __ldg(rb + i);
+      }
+      tmem_st32(trow + 256 + 64 * h, *reinterpret_cast<float(*)[32]>(x));
+      tmem_st32(trow + 256 + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
+      st64(qp, x);  // push the layer input (same thread read this slot earlier)
+      row_to_image(xs + h * kTile, r, x);
+      row_to_image(xs + (2 + h) * kTile, r, q);
+      if (l + 1 < L) {
+        qp = qptr(l + 1);
+        ld64(q, qp);  // prefetch x_{l+1}[t - d_{l+1}]; lands during this layer's MMAs
+      }
+      tmem_wait_st();
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(a_ready);
+
+      // ---- gate ----
+      mbar_wait(acc_full, acc_par);
+      acc_par ^= 1;
+      tc_fence_after();
+      const float* bd = a.dil_b + (size_t)l * 2 * kD;
+      uint8_t* zchunk = zdst + (size_t)(2 * l + h) * kTile;
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        float at[32], as[32];
+        tmem_ld32(trow + 64 * h + 32 * qq, at);
+        tmem_ld32(trow + 128 + 64 * h + 32 * qq, as);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const int j = 64 * h + 32 * qq + i;
+          float z0 = tanh_fast(at[i] + __ldg(bd + j)) *
+                     fmaf(0.5f, tanh_fast(0.5f * (as[i] + __ldg(bd + kD + j))), 0.5f);
+          float z1 = tanh_fast(at[i + 1] + __ldg(bd + j + 1)) *
+                     fmaf(0.5f, tanh_fast(0.5f * (as[i + 1] + __ldg(bd + kD + j + 1))), 0.5f);
+          pk[i >> 1] = pack_bf16(z0, z1);
+        }
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const uint32_t off = swz(r, 4 * qq + p);
+          st_shared_v4(zs + h * kTile + off, pk[4 * p], pk[4 * p + 1], pk[4 * p + 2], pk[4 * p + 3]);
+          *reinterpret_cast<uint4*>(zchunk + off) =
+              make_uint4(pk[4 * p], pk[4 * p + 1], pk[4 * p + 2], pk[4 * p + 3]);
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      if (l + 1 < L) mbar_arrive(z_ready);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
+// ---- generic [128 x BN] tile GEMM over pre-swizzled A/B images ----------------------
+struct GemmArgs {
+  const uint8_t* a;  // [mtiles][kch][16 KB]
+  const uint8_t* b;  // [ntiles][kch][BN * 128 B]
+  int kch;
+  const float* bias;  // [N]
+  uint8_t* out_img;   // epi 0: [mtiles][N/64][16 KB]
+  int n_total;
+  // epi 1 (head2 + selection)
+  float* logits;  // [B][A] for this step or null
+  int32_t* out_cls;
+  int32_t* cls_next;
+  const int32_t* next_inputs;  // teacher row for the next step or null
+  int B, A, mode;
+  uint32_t seed;
+  int64_t stream_offset;
+  int64_t t;
+};
+
+template <int BN>
+constexpr int gemm_stages() {
+  return BN == 256 ? 3 : 4;
+}
+template <int BN>
+constexpr uint32_t gemm_stage_bytes() {
+  return kTile + BN * 128;
+}
+template <int BN>
+constexpr size_t gemm_smem() {
+  return 1024 + gemm_stages<BN>() * gemm_stage_bytes<BN>() + 256 + 4 * 128 * 4 * 2;
+}
+
+__device__ __forceinline__ float gumbel_score(float v, uint32_t prefix, int cls) {
+  const float u = noise_uniform(prefix, (uint32_t)cls);
+  return v - __logf(-__logf(u));
+}
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(GemmArgs g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  constexpr int S = gemm_stages<BN>();
+  constexpr uint32_t SB = gemm_stage_bytes<BN>();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * SB);
+  uint64_t* full = bars;
+  uint64_t* empty = bars + S;
+  uint64_t* acc_full = bars + 2 * S;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * S + 1);
+  float* xch = reinterpret_cast<float*>(smem + S * SB + 256);  // [4][128][2] exchange
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mt = blockIdx.x, nt = blockIdx.y;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, BN);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint8_t* abase = g.a + (size_t)mt * g.kch * kTile;
+      const uint8_t* bbase = g.b + (size_t)nt * g.kch * (BN * 128);
+      for (int kc = 0; kc < g.kch; ++kc) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], SB);
+        bulk_g2s(smem + stage * SB, abase + (size_t)kc * kTile, kTile, &full[stage]);
+        bulk_g2s(smem + stage * SB + kTile, bbase + (size_t)kc * (BN * 128), BN * 128, &full[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t id = idesc_bf16(128, BN);
+      const uint32_t s0 = smem_u32(smem);
+      for (int kc = 0; kc < g.kch; ++kc) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16(tmem, sdesc_sw128(s0 + stage * SB + kk * 32),
+                   sdesc_sw128(s0 + stage * SB + kTile + kk * 32), id, (kc | kk) != 0);
+        mma_commit(&empty[stage]);
+        if (++stage == S) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      mma_commit(acc_full);
+    }
+    __syncwarp();
+  } else {
+    const int sub = warp & 3, h = (warp - 2) >> 2;
+    const int r = sub * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    constexpr int HALF = BN / 2;  // columns per thread
+    if (EPI == 0) {
+      // v = ReLU(acc + bias) -> bf16 image chunk (mt, (nt*BN + h*HALF)/64 ...)
+#pragma unroll
+      for (int cc = 0; cc < HALF / 64; ++cc) {
+        float v[64];
+        tmem_ld32(trow + h * HALF + 64 * cc, *reinterpret_cast<float(*)[32]>(v));
+        tmem_ld32(trow + h * HALF + 64 * cc + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+        tmem_wait_ld();
+        const int n0 = nt * BN + h * HALF + 64 * cc;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + __ldg(g.bias + n0 + i), 0.f);
+        uint8_t* dst = g.out_img + ((size_t)mt * (g.n_total / 64) + n0 / 64) * kTile;
+#pragma unroll
+        for (int p = 0; p < 8; ++p)
+          *reinterpret_cast<uint4*>(dst + swz(r, p)) =
+              make_uint4(pack_bf16(v[8 * p], v[8 * p + 1]), pack_bf16(v[8 * p + 2], v[8 * p + 3]),
+                         pack_bf16(v[8 * p + 4], v[8 * p + 5]), pack_bf16(v[8 * p + 6], v[8 * p + 7]));
+      }
+    } else {
+      // head2 + selection; this thread owns columns [h*HALF, (h+1)*HALF) of row r
+      const int stream = mt * 128 + r;
+      const uint32_t prefix =
+          noise_prefix(g.seed, (uint32_t)(g.stream_offset + stream), (uint32_t)g.t);
+      const int cbase = h * HALF;
+      float* lrow = g.logits ? g.logits + (size_t)stream * g.A : nullptr;
+      float best = -INFINITY, mx = -INFINITY;
+      int bi = g.A;
+#pragma unroll 1
+      for (int cc = 0; cc < HALF / 32; ++cc) {
+        float v[32];
+        tmem_ld32(trow + cbase + 32 * cc, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int col = cbase + 32 * cc + i;
+          v[i] += __ldg(g.bias + col);
+          mx = fmaxf(mx, v[i]);
+          float sc = v[i];
+          if (g.mode == FW_SAMPLE_GUMBEL) sc = gumbel_score(v[i], prefix, col);
+          if (sc > best) {
+            best = sc;
+            bi = col;
+          }
+        }
+        if (lrow) {
+          float4* d4 = reinterpret_cast<float4*>(lrow + cbase + 32 * cc);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        }
+      }
+      float* xb = xch;              // best score  [2][128]
+      int* xi = reinterpret_cast<int*>(xch + 256);  // best index [2][128]
+      float* xm = xch + 512;        // max [2][128]
+      float* xs = xch + 768;        // sum [2][128]
+      xb[h * 128 + r] = best;
+      xi[h * 128 + r] = bi;
+      xm[h * 128 + r] = mx;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      int choice;
+      if (g.mode != FW_SAMPLE_INVCDF) {
+        const float ob = xb[(h ^ 1) * 128 + r];
+        const int oi = xi[(h ^ 1) * 128 + r];
+        choice = (ob > best || (ob == best && oi < bi)) ? oi : bi;
+      } else {
+        const float m = fmaxf(mx, xm[(h ^ 1) * 128 + r]);
+        float part = 0.f;
+        for (int cc = 0; cc < HALF / 32; ++cc) {
+          float v[32];
+          tmem_ld32(trow + cbase + 32 * cc, v);
+          tmem_wait_ld();
+          for (int i = 0; i < 32; ++i) part += __expf(v[i] + __ldg(g.bias + cbase + 32 * cc + i) - m);
+        }
+        xs[h * 128 + r] = part;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const float s0 = xs[r], total = s0 + xs[128 + r];
+        const float thr = noise_uniform(prefix, kUniformClass) * total;
+        float run = (h == 0) ? 0.f : s0;
+        int found = g.A;
+        for (int cc = 0; cc < HALF / 32 && found == g.A; ++cc) {
+          float v[32];
+          tmem_ld32(trow + cbase + 32 * cc, v);
+          tmem_wait_ld();
+          for (int i = 0; i < 32; ++i) {
+            run += __expf(v[i] + __ldg(g.bias + cbase + 32 * cc + i) - m);
+            if (found == g.A && run > thr) found = cbase + 32 * cc + i;
+          }
+        }
+        xi[h * 128 + r] = found;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        const int f0 = xi[r], f1 = xi[128 + r];
+        choice = f0 < g.A ? f0 : (f1 < g.A ? f1 : g.A - 1);
+      }
+      if (h == 0) {
+        g.out_cls[stream] = choice;
+        g.cls_next[stream] = g.next_inputs ? g.next_inputs[stream] : choice;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, BN);
+}
+
+// ---- host-side packing ---------------------------------------------------------------
+uint16_t bf16_bits(float f) {
+  __nv_bfloat16 b = __float2bfloat16_rn(f);
+  uint16_t u;
+  std::memcpy(&u, &b, 2);
+  return u;
+}
+
+// Rows [0, nrows) of the (row, k) -> value function, K slice [k0, k0+64), as a swizzled image.
+template <typename F>
+void pack_image(uint8_t* dst, int nrows, int k0, F val) {
+  for (int r = 0; r < nrows; ++r)
+    for (int k = 0; k < 64; ++k) {
+      const size_t off = (size_t)(r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) ^ (r & 7))) << 4) + (k & 7) * 2;
+      const uint16_t b = bf16_bits(val(r, k0 + k));
+      std::memcpy(dst + off, &b, 2);
+    }
+}
+
+template <typename T>
+int dev_alloc(T** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), bytes);
+  if (e != cudaSuccess) {
+    set_error(std::string("tcgen05 path allocation: ") + cudaGetErrorString(e));
+    return FW_ERR_CUDA;
+  }
+  return FW_OK;
+}
+
+int upload_bytes(uint8_t** dst, const std::vector<uint8_t>& src) {
+  int rc = dev_alloc(dst, src.size());
+  if (rc) return rc;
+  cudaError_t e = cudaMemcpy(*dst, src.data(), src.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    set_error(std::string("tcgen05 weight upload: ") + cudaGetErrorString(e));
+    return FW_ERR_CUDA;
+  }
+  return FW_OK;
+}
+
+template <typename K>
+cudaError_t set_smem(K kernel, size_t bytes) {
+  return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+constexpr size_t kChainSmem = 1024 + 6 * kTile + kChainStages * kChainStage + 128;
+
+}  // namespace
+
+bool tc_supported(const CellDims& d, int batch, std::string* why) {
+  auto no = [&](const char* m) {
+    if (why) *why = m;
+    return false;
+  };
+  if (d.dtype != FW_DTYPE_BF16) return no("needs bf16 weights");
+  if (d.R != kR || d.D != kD) return no("needs residual = dilation = 128 channels");
+  if (d.S % 128 || d.H % 128 || d.S > 2048 || d.H > 2048) return no("needs skip/head multiples of 128");
+  if (d.A != 256) return no("needs 256 classes");
+  if (batch % 128) return no("needs a batch that is a multiple of 128 streams");
+  return true;
+}
+
+int tc_create(Handle& h, const fw_cell_desc* desc) {
+  const CellDims& d = h.dims;
+  const int L = d.L, S = d.S, H = d.H, A = d.A;
+  TcState* tc = new TcState();
+  h.tc = tc;
+  tc->ntile = h.batch / 128;
+  // chain weights: per layer 4 dil chunks of [256 n][64 k] over K = [x_t | x_{t-d}], 2 res chunks
+  {
+    std::vector<uint8_t> img((size_t)L * kLayerBytes, 0);
+    for (int l = 0; l < L; ++l) {
+      uint8_t* base = img.data() + (size_t)l * kLayerBytes;
+      const float* w0 = desc->dil_w + ((size_t)l * 2 + 0) * 2 * kD * kR;
+      const float* w1 = desc->dil_w + ((size_t)l * 2 + 1) * 2 * kD * kR;
+      for (int c = 0; c < 4; ++c)
+        pack_image(base + c * kDilChunk, 256, c * 64, [&](int n, int k) {
+          return k < kR ? w0[(size_t)n * kR + k] : w1[(size_t)n * kR + (k - kR)];
+        });
+      const float* wr = desc->res_w + (size_t)l * kR * kD;
+      for (int c = 0; c < 2; ++c)
+        pack_image(base + 4 * kDilChunk + c * kResChunk, 128, c * 64,
+                   [&](int n, int k) { return wr[(size_t)n * kD + k]; });
+    }
+    if (int rc = upload_bytes(&tc->wchain, img)) return rc;
+  }
+  const int kskip = L * kD / 64;
+  {
+    std::vector<uint8_t> img((size_t)(S / 128) * kskip * kTile);
+    for (int nb = 0; nb < S / 128; ++nb)
+      for (int kc = 0; kc < kskip; ++kc)
+        pack_image(img.data() + ((size_t)nb * kskip + kc) * kTile, 128, kc * 64, [&](int n, int k) {
+          const int l = k / kD, j = k % kD;
+          return desc->skip_w[((size_t)l * S + nb * 128 + n) * kD + j];
+        });
+    if (int rc = upload_bytes(&tc->wskip, img)) return rc;
+  }
+  {
+    std::vector<uint8_t> img((size_t)(H / 128) * (S / 64) * kTile);
+    for (int nb = 0; nb < H / 128; ++nb)
+      for (int kc = 0; kc < S / 64; ++kc)
+        pack_image(img.data() + ((size_t)nb * (S / 64) + kc) * kTile, 128, kc * 64,
+                   [&](int n, int k) { return desc->head1_w[(size_t)(nb * 128 + n) * S + k]; });
+    if (int rc = upload_bytes(&tc->wh1, img)) return rc;
+  }
+  {
+    std::vector<uint8_t> img((size_t)(H / 64) * A * 128);
+    for (int kc = 0; kc < H / 64; ++kc)
+      pack_image(img.data() + (size_t)kc * A * 128, A, kc * 64,
+                 [&](int n, int k) { return desc->head2_w[(size_t)n * H + k]; });
+    if (int rc = upload_bytes(&tc->wh2, img)) return rc;
+  }
+  {
+    std::vector<float> bsum(S, 0.f);
+    for (int l = 0; l < L; ++l)
+      for (int n = 0; n < S; ++n) bsum[n] += __bfloat162float(__float2bfloat16_rn(desc->skip_b[(size_t)l * S + n]));
+    if (int rc = dev_alloc(&tc->skip_bsum, sizeof(float) * S)) return rc;
+    cudaMemcpy(tc->skip_bsum, bsum.data(), sizeof(float) * S, cudaMemcpyHostToDevice);
+  }
+  if (int rc = dev_alloc(&tc->zimg, (size_t)tc->ntile * kskip * kTile)) return rc;
+  if (int rc = dev_alloc(&tc->simg, (size_t)tc->ntile * (S / 64) * kTile)) return rc;
+  if (int rc = dev_alloc(&tc->himg, (size_t)tc->ntile * (H / 64) * kTile)) return rc;
+  if (int rc = dev_alloc(&tc->cls, sizeof(int32_t) * h.batch)) return rc;
+  cudaError_t e = set_smem(chain_kernel, kChainSmem);
+  if (e == cudaSuccess) e = set_smem(gemm_kernel<128, 0>, gemm_smem<128>());
+  if (e == cudaSuccess) e = set_smem(gemm_kernel<256, 1>, gemm_smem<256>());
+  if (e != cudaSuccess) {
+    set_error(std::string("tcgen05 kernel attributes: ") + cudaGetErrorString(e));
+    return FW_ERR_CUDA;
+  }
+  return FW_OK;
+}
+
+void tc_destroy(Handle& h) {
+  TcState* tc = h.tc;
+  if (!tc) return;
+  void* ptrs[] = {tc->wchain, tc->wskip, tc->wh1, tc->wh2, tc->skip_bsum,
+                  tc->zimg, tc->simg, tc->himg, tc->cls};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete tc;
+  h.tc = nullptr;
+}
+
+cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64_t* launches) {
+  TcState* tc = h.tc;
+  const CellDims& d = h.dims;
+  const int B = h.batch, L = d.L, S = d.S, H = d.H;
+  cudaError_t e = cudaMemcpyAsync(tc->cls, run.inputs, sizeof(int32_t) * B,
+                                  cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) return e;
+  ChainArgs ca{B, L, 0, h.d_dil, h.d_qoff, h.d_queue, tc->wchain, h.w.embed, h.w.dil_b,
+               h.w.res_b, tc->cls, tc->zimg};
+  GemmArgs skip{};
+  skip.a = tc->zimg;
+  skip.b = tc->wskip;
+  skip.kch = L * kD / 64;
+  skip.bias = tc->skip_bsum;
+  skip.out_img = tc->simg;
+  skip.n_total = S;
+  GemmArgs h1{};
+  h1.a = tc->simg;
+  h1.b = tc->wh1;
+  h1.kch = S / 64;
+  h1.bias = h.w.h1_b;
+  h1.out_img = tc->himg;
+  h1.n_total = H;
+  GemmArgs h2{};
+  h2.a = tc->himg;
+  h2.b = tc->wh2;
+  h2.kch = H / 64;
+  h2.bias = h.w.h2_b;
+  h2.B = B;
+  h2.A = d.A;
+  h2.mode = run.mode;
+  h2.seed = run.seed;
+  h2.stream_offset = run.stream_offset;
+  h2.cls_next = tc->cls;
+  const dim3 gskip(tc->ntile, S / 128), gh1(tc->ntile, H / 128), gh2(tc->ntile, 1);
+  for (int i = 0; i < run.n_steps; ++i) {
+    ca.t = run.t0 + i;
+    chain_kernel<<<tc->ntile, kThreads, kChainSmem, st>>>(ca);
+    gemm_kernel<128, 0><<<gskip, kThreads, gemm_smem<128>(), st>>>(skip);
+    gemm_kernel<128, 0><<<gh1, kThreads, gemm_smem<128>(), st>>>(h1);
+    h2.t = run.t0 + i;
+    h2.logits = (run.logits && i < run.n_logit_steps) ? run.logits + (size_t)i * B * d.A : nullptr;
+    h2.out_cls = run.out + (size_t)i * B;
+    h2.next_inputs = (i + 1 < run.n_inputs) ? run.inputs + (size_t)(i + 1) * B : nullptr;
+    gemm_kernel<256, 1><<<gh2, kThreads, gemm_smem<256>(), st>>>(h2);
+  }
+  *launches = 4 * (int64_t)run.n_steps;
+  return cudaGetLastError();
+}
+
 }  // namespace fw
