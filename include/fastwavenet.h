@@ -170,6 +170,10 @@ int fw_kernel_kind(const fw_handle* h, int32_t* out);
 int fw_last_launch_count(const fw_handle* h, int64_t* out);
 int fw_destroy(fw_handle* h);
 const char* fw_last_error(void);
+/* Diagnostics: record per-layer clock64() phase timestamps of CTA 0 of the
+ * tcgen05 chain kernel into d_trace [n_layers][16] (NULL disables). Not part
+ * of the reference's interface; used by tools/trace_chain.py. */
+int fw_debug_trace(fw_handle* h, int64_t* d_trace);
 /* Library ABI version (major*100 + minor). */
 int32_t fw_version(void);
 

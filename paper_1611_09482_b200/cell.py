@@ -78,6 +78,8 @@ class CellConfig:
             raise ValueError("bias must be 'zero' or 'fan_in'")
         if not 0 <= self.init_seed < 2**64:
             raise ValueError("init_seed must fit in an unsigned 64-bit integer")
+        if self.dilation_base ** (self.layers_per_block - 1) >= 2**30:
+            raise ValueError("dilation_base**(layers_per_block-1) must be below 2**30")
 
     @property
     def total_layers(self) -> int:

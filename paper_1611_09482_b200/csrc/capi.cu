@@ -473,6 +473,14 @@ int fw_reset(fw_handle* fh, void* stream) {
   return FW_OK;
 }
 
+int fw_debug_trace(fw_handle* fh, int64_t* d_trace) {
+  int rc = check_handle(fh, false);
+  if (rc) return rc;
+  if (fh->h.kernel != FW_KERNEL_TCGEN05) return invalid("phase trace needs the tcgen05 path");
+  tc_set_trace(fh->h, reinterpret_cast<long long*>(d_trace));
+  return FW_OK;
+}
+
 int fw_step_index(const fw_handle* fh, int64_t* out) {
   if (!fh || !out) return invalid("null argument");
   *out = fh->h.t;

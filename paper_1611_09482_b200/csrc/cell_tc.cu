@@ -33,7 +33,7 @@ namespace fw {
 
 struct TcState {
   int ntile = 0;
-  uint8_t* wchain = nullptr;  // per layer: 4 dil chunks [256][64] + 2 res chunks [128][64]
+  uint8_t* wchain = nullptr;  // per layer: 10 chunks [128][64] in MMA issue order
   uint8_t* wskip = nullptr;   // [S/128][L*D/64] chunks of [128][64]
   uint8_t* wh1 = nullptr;     // [H/128][S/64] chunks of [128][64]
   uint8_t* wh2 = nullptr;     // [H/64] chunks of [A=256][64]
@@ -42,30 +42,43 @@ struct TcState {
   uint8_t* simg = nullptr;    // [ntile][S/64][16 KB]
   uint8_t* himg = nullptr;    // [ntile][H/64][16 KB]
   int32_t* cls = nullptr;     // [B]
+  int has_dil_bias = 1, has_res_bias = 1;
+  long long* trace = nullptr;  // device buffer [L][kTraceSlots] (debug)
 };
+
+void tc_set_trace(Handle& h, long long* trace) {
+  if (h.tc) h.tc->trace = trace;
+}
 
 namespace {
 
 using namespace ptx;
 
 constexpr int kThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
-constexpr int kChainStages = 4;
-constexpr uint32_t kChainStage = 32768;
-constexpr uint32_t kDilChunk = 32768;   // [256 rows][64] bf16
-constexpr uint32_t kResChunk = 16384;   // [128 rows][64] bf16
-constexpr uint32_t kLayerBytes = 4 * kDilChunk + 2 * kResChunk;
-constexpr uint32_t kTile = 16384;       // [128 rows][64] bf16 activation chunk
+constexpr int kChainStages = 8;
+constexpr uint32_t kChunk = 16384;  // one [128 rows][64] bf16 operand image
+constexpr int kChunksPerLayer = 10;  // 8 dil (2 N-halves x 4 K-chunks) + 2 res
+constexpr uint32_t kLayerBytes = kChunksPerLayer * kChunk;
+constexpr uint32_t kTile = 16384;    // [128 rows][64] bf16 activation chunk
 constexpr int kR = 128, kD = 128;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
   return reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(p) + 1023) & ~uintptr_t(1023));
 }
 
+constexpr int kMaxChainLayers = 128;
+
+// Device-side phase trace (CTA 0 only, clock64 cycles), enabled by fw_debug_trace.
+// Per layer kTraceSlots entries; see tools/trace_chain.py for the slot meanings.
+constexpr int kTraceSlots = 16;
+enum TraceSlot {
+  T_MMA_XD = 0, T_MMA_XT, T_MMA_ACC0, T_MMA_ACC1, T_MMA_Z0, T_MMA_Z1, T_MMA_XFULL, T_MMA_WWAIT,
+  T_EPI_A, T_EPI_XFULL, T_EPI_XT, T_EPI_GLOBAL, T_EPI_ACC0, T_EPI_Z0, T_EPI_ACC1, T_EPI_Z1
+};
+
 struct ChainArgs {
   int B, L;
-  int64_t t;
-  const int* dil;
-  const int64_t* qoff;
+  int64_t qbase[kMaxChainLayers];  // element offset of slot (t mod d_l) of layer l's ring
   float* queue;
   const uint8_t* w;
   const float* embed;  // [A][128]
@@ -73,7 +86,13 @@ struct ChainArgs {
   const float* res_b;  // [L][128]
   const int32_t* cls;  // [B]
   uint8_t* zimg;
+  int has_dil_bias, has_res_bias;
+  long long* trace;  // [L][kTraceSlots] or null
 };
+
+__device__ __forceinline__ void trace_at(const ChainArgs& a, int l, int slot, long long v) {
+  if (a.trace != nullptr && blockIdx.x == 0) a.trace[l * kTraceSlots + slot] = v;
+}
 
 __device__ __forceinline__ void ld64(float (&v)[64], const float* p) {
   const float4* q = reinterpret_cast<const float4*>(p);
@@ -100,19 +119,36 @@ __device__ __forceinline__ void row_to_image(uint32_t img_saddr, int r, const fl
                  pack_bf16(v[8 * p + 6], v[8 * p + 7]));
 }
 
+// Chain kernel: one 128-stream tile per CTA, all layers of one step.
+//
+// TMEM columns: acc0 [0,128)  = dil N-half 0 (tanh rows 0..63 | sigmoid rows 0..63)
+//               acc1 [128,256) = dil N-half 1 (tanh rows 64..127 | sigmoid rows 64..127)
+//               x    [256,384) = residual stream x_l (fp32), the res MMA accumulates onto it.
+// Shared: X0,X1 = bf16 x_t (K 0..127), X2,X3 = bf16 x_{t-d} (K 128..255), Z0,Z1 = bf16 z,
+//         8-stage ring of 16 KB weight chunks.
+// Per layer the MMA thread issues, in the producer's streaming order:
+//   [xd_ready] dil h0 kc2,kc3 ; dil h1 kc2,kc3      (x_{t-d} half: independent of x_l)
+//   [xt_ready] dil h0 kc0,kc1 -> acc0_full ; dil h1 kc0,kc1 -> acc1_full
+//   [z0_ready] res kc0 ; [z1_ready] res kc1 -> x_full
+// so the x_{t-d} half of the next layer's GEMM overlaps the residual epilogue, and the
+// second N-half overlaps the first half's gate.
 __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* X = smem;                  // 4 chunks: x_t[0:64], x_t[64:128], x_{t-d}[0:64], x_{t-d}[64:128]
+  uint8_t* X = smem;                  // 4 chunks
   uint8_t* Z = smem + 4 * kTile;      // 2 chunks
-  uint8_t* ring = smem + 6 * kTile;   // kChainStages x 32 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kChainStages * kChainStage);
+  uint8_t* ring = smem + 6 * kTile;   // kChainStages x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kChainStages * kChunk);
   uint64_t* full = bars;
   uint64_t* empty = bars + kChainStages;
-  uint64_t* a_ready = bars + 2 * kChainStages;
-  uint64_t* z_ready = a_ready + 1;
-  uint64_t* acc_full = a_ready + 2;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(a_ready + 3);
+  uint64_t* xd_ready = bars + 2 * kChainStages;
+  uint64_t* xt_ready = xd_ready + 1;
+  uint64_t* z0_ready = xd_ready + 2;
+  uint64_t* z1_ready = xd_ready + 3;
+  uint64_t* acc0_full = xd_ready + 4;
+  uint64_t* acc1_full = xd_ready + 5;
+  uint64_t* x_full = xd_ready + 6;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xd_ready + 7);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
@@ -123,9 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    mbar_init(a_ready, 256);
-    mbar_init(z_ready, 256);
-    mbar_init(acc_full, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(xd_ready + i, 256);
+    for (int i = 4; i < 7; ++i) mbar_init(xd_ready + i, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -135,18 +170,16 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- weight producer ----
+    if (lane == 0) {  // ---- weight producer: streams chunks in MMA order ----
       int stage = 0;
       uint32_t phase = 0;
       for (int l = 0; l < L; ++l) {
         const uint8_t* wl = a.w + (size_t)l * kLayerBytes;
-        const int nchunk = (l + 1 < L) ? 6 : 4;
-        for (int c = 0; c < nchunk; ++c) {
-          const uint32_t bytes = c < 4 ? kDilChunk : kResChunk;
-          const uint8_t* src = c < 4 ? wl + c * kDilChunk : wl + 4 * kDilChunk + (c - 4) * kResChunk;
+        const int n = (l + 1 < L) ? kChunksPerLayer : 8;
+        for (int c = 0; c < n; ++c) {
           mbar_wait(&empty[stage], phase ^ 1);
-          mbar_arrive_expect_tx(&full[stage], bytes);
-          bulk_g2s(ring + stage * kChainStage, src, bytes, &full[stage]);
+          mbar_arrive_expect_tx(&full[stage], kChunk);
+          bulk_g2s(ring + stage * kChunk, wl + (size_t)c * kChunk, kChunk, &full[stage]);
           if (++stage == kChainStages) {
             stage = 0;
             phase ^= 1;
@@ -157,127 +190,162 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer ----
       int stage = 0;
-      uint32_t phase = 0, a_par = 0, z_par = 0;
-      const uint32_t id_dil = idesc_bf16(128, 256), id_res = idesc_bf16(128, 128);
+      uint32_t phase = 0, par = 0;
+      const uint32_t id = idesc_bf16(128, 128);
       const uint32_t xs = smem_u32(X), zs = smem_u32(Z), rs = smem_u32(ring);
-      for (int l = 0; l < L; ++l) {
-        mbar_wait(a_ready, a_par);
-        a_par ^= 1;
+      long long wwait = 0;
+      auto chunk = [&](uint32_t d_tmem, uint32_t a_saddr, bool first) {
+        const long long w0 = clock64();
+        mbar_wait(&full[stage], phase);
+        wwait += clock64() - w0;
         tc_fence_after();
-        for (int c = 0; c < 4; ++c) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_bf16(tmem, sdesc_sw128(xs + c * kTile + kk * 32),
-                     sdesc_sw128(rs + stage * kChainStage + kk * 32), id_dil, (c | kk) != 0);
-          mma_commit(&empty[stage]);
-          if (++stage == kChainStages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16(d_tmem, sdesc_sw128(a_saddr + kk * 32),
+                   sdesc_sw128(rs + stage * kChunk + kk * 32), id, (first && kk == 0) ? 0u : 1u);
+        mma_commit(&empty[stage]);
+        if (++stage == kChainStages) {
+          stage = 0;
+          phase ^= 1;
         }
-        mma_commit(acc_full);
+      };
+      for (int l = 0; l < L; ++l) {
+        mbar_wait(xd_ready, par);
+        trace_at(a, l, T_MMA_XD, clock64());
+        tc_fence_after();
+        chunk(tmem + 0, xs + 2 * kTile, true);
+        chunk(tmem + 0, xs + 3 * kTile, false);
+        chunk(tmem + 128, xs + 2 * kTile, true);
+        chunk(tmem + 128, xs + 3 * kTile, false);
+        mbar_wait(xt_ready, par);
+        trace_at(a, l, T_MMA_XT, clock64());
+        tc_fence_after();
+        chunk(tmem + 0, xs + 0 * kTile, false);
+        chunk(tmem + 0, xs + 1 * kTile, false);
+        mma_commit(acc0_full);
+        trace_at(a, l, T_MMA_ACC0, clock64());
+        chunk(tmem + 128, xs + 0 * kTile, false);
+        chunk(tmem + 128, xs + 1 * kTile, false);
+        mma_commit(acc1_full);
+        trace_at(a, l, T_MMA_ACC1, clock64());
         if (l + 1 < L) {
-          mbar_wait(z_ready, z_par);
-          z_par ^= 1;
+          mbar_wait(z0_ready, par);
+          trace_at(a, l, T_MMA_Z0, clock64());
           tc_fence_after();
-          for (int c = 0; c < 2; ++c) {
-            mbar_wait(&full[stage], phase);
-            tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              mma_bf16(tmem + 256, sdesc_sw128(zs + c * kTile + kk * 32),
-                       sdesc_sw128(rs + stage * kChainStage + kk * 32), id_res, 1);
-            mma_commit(&empty[stage]);
-            if (++stage == kChainStages) {
-              stage = 0;
-              phase ^= 1;
-            }
-          }
-          mma_commit(acc_full);
+          chunk(tmem + 256, zs + 0 * kTile, false);
+          mbar_wait(z1_ready, par);
+          trace_at(a, l, T_MMA_Z1, clock64());
+          tc_fence_after();
+          chunk(tmem + 256, zs + 1 * kTile, false);
+          mma_commit(x_full);
+          trace_at(a, l, T_MMA_XFULL, clock64());
         }
+        trace_at(a, l, T_MMA_WWAIT, wwait);
+        par ^= 1;
       }
     }
     __syncwarp();
-  } else {  // ---- epilogue warps 2..9 ----
+  } else {  // ---- epilogue warps 2..9: thread = (row r, half h) ----
     const int sub = warp & 3, h = (warp - 2) >> 2;
     const int r = sub * 32 + lane;
     const int stream = tile * 128 + r;
     const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
     const uint32_t xs = smem_u32(X), zs = smem_u32(Z);
     const int c = a.cls[stream];
-    uint32_t acc_par = 0;
+    uint32_t par = 0;
     float q[64];
-    auto qptr = [&](int l) {
-      return a.queue + a.qoff[l] + (size_t)(a.t % a.dil[l]) * a.B * kR + (size_t)stream * kR + 64 * h;
-    };
+    const bool tr = (warp == 2 && lane == 0);
+    auto qptr = [&](int l) { return a.queue + a.qbase[l] + (size_t)stream * kR + 64 * h; };
     float* qp = qptr(0);
     ld64(q, qp);
     uint8_t* zdst = a.zimg + (size_t)tile * (L * 2) * kTile;
     for (int l = 0; l < L; ++l) {
-      // ---- pop/push + operand build ----
+      // (a) x_{t-d} half of the operand: independent of this step's residual stream
+      row_to_image(xs + (2 + h) * kTile, r, q);
+      fence_proxy_async();
+      mbar_arrive(xd_ready);
+      if (tr) trace_at(a, l, T_EPI_A, clock64());
+      // (b) x_l: embedding at l = 0, else the TMEM residual stream (+ the pending bias)
       float x[64];
       if (l == 0) {
         ld64(x, a.embed + (size_t)c * kR + 64 * h);
+        tmem_st32(trow + 256 + 64 * h, *reinterpret_cast<float(*)[32]>(x));
+        tmem_st32(trow + 256 + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
       } else {
-        mbar_wait(acc_full, acc_par);
-        acc_par ^= 1;
+        mbar_wait(x_full, par ^ 1);
+        if (tr) trace_at(a, l, T_EPI_XFULL, clock64());
         tc_fence_after();
         tmem_ld32(trow + 256 + 64 * h, *reinterpret_cast<float(*)[32]>(x));
         tmem_ld32(trow + 256 + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
         tmem_wait_ld();
-        const float* rb = a.res_b + (size_t)(l - 1) * kR + 64 * h;
+        if (a.has_res_bias) {
+          const float4* rb = reinterpret_cast<const float4*>(a.res_b + (size_t)(l - 1) * kR + 64 * h);
 #pragma unroll
-        for (int i = 0; i < 64; ++i) x[i] += __ldg(rb + i);
+          for (int i = 0; i < 16; ++i) {
+            const float4 b = __ldg(rb + i);
+            x[4 * i] += b.x;
+            x[4 * i + 1] += b.y;
+            x[4 * i + 2] += b.z;
+            x[4 * i + 3] += b.w;
+          }
+          tmem_st32(trow + 256 + 64 * h, *reinterpret_cast<float(*)[32]>(x));
+          tmem_st32(trow + 256 + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
+        }
       }
-      tmem_st32(trow + 256 + 64 * h, *reinterpret_cast<float(*)[32]>(x));
-      tmem_st32(trow + 256 + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
-      st64(qp, x);  // push the layer input (same thread read this slot earlier)
       row_to_image(xs + h * kTile, r, x);
-      row_to_image(xs + (2 + h) * kTile, r, q);
-      if (l + 1 < L) {
-        qp = qptr(l + 1);
-        ld64(q, qp);  // prefetch x_{l+1}[t - d_{l+1}]; lands during this layer's MMAs
-      }
       tmem_wait_st();
       fence_proxy_async();
       tc_fence_before();
-      mbar_arrive(a_ready);
-
-      // ---- gate ----
-      mbar_wait(acc_full, acc_par);
-      acc_par ^= 1;
-      tc_fence_after();
+      mbar_arrive(xt_ready);
+      if (tr) trace_at(a, l, T_EPI_XT, clock64());
+      // global traffic after the fences so they never wait on it
+      st64(qp, x);  // push the layer input into slot t mod d (read earlier by this thread)
+      if (l + 1 < L) {
+        qp = qptr(l + 1);
+        ld64(q, qp);  // prefetch x_{l+1}[t - d_{l+1}]
+      }
+      if (tr) trace_at(a, l, T_EPI_GLOBAL, clock64());
+      // (c,d) gate of N-half hh -> z columns 64*hh + [32h, 32h+32)
       const float* bd = a.dil_b + (size_t)l * 2 * kD;
-      uint8_t* zchunk = zdst + (size_t)(2 * l + h) * kTile;
+      uint8_t* zrow = zdst + (size_t)(2 * l) * kTile;
 #pragma unroll
-      for (int qq = 0; qq < 2; ++qq) {
+      for (int hh = 0; hh < 2; ++hh) {
+        mbar_wait(hh == 0 ? acc0_full : acc1_full, par);
+        if (tr) trace_at(a, l, hh == 0 ? T_EPI_ACC0 : T_EPI_ACC1, clock64());
+        tc_fence_after();
         float at[32], as[32];
-        tmem_ld32(trow + 64 * h + 32 * qq, at);
-        tmem_ld32(trow + 128 + 64 * h + 32 * qq, as);
+        tmem_ld32(trow + 128 * hh + 32 * h, at);
+        tmem_ld32(trow + 128 * hh + 64 + 32 * h, as);
         tmem_wait_ld();
+        if (a.has_dil_bias) {
+          const int j0 = 64 * hh + 32 * h;
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            at[i] += __ldg(bd + j0 + i);
+            as[i] += __ldg(bd + kD + j0 + i);
+          }
+        }
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
-          const int j = 64 * h + 32 * qq + i;
-          float z0 = tanh_fast(at[i] + __ldg(bd + j)) *
-                     fmaf(0.5f, tanh_fast(0.5f * (as[i] + __ldg(bd + kD + j))), 0.5f);
-          float z1 = tanh_fast(at[i + 1] + __ldg(bd + j + 1)) *
-                     fmaf(0.5f, tanh_fast(0.5f * (as[i + 1] + __ldg(bd + kD + j + 1))), 0.5f);
+          const float z0 = tanh_fast(at[i]) * fmaf(0.5f, tanh_fast(0.5f * as[i]), 0.5f);
+          const float z1 = tanh_fast(at[i + 1]) * fmaf(0.5f, tanh_fast(0.5f * as[i + 1]), 0.5f);
           pk[i >> 1] = pack_bf16(z0, z1);
         }
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-          const uint32_t off = swz(r, 4 * qq + p);
-          st_shared_v4(zs + h * kTile + off, pk[4 * p], pk[4 * p + 1], pk[4 * p + 2], pk[4 * p + 3]);
-          *reinterpret_cast<uint4*>(zchunk + off) =
+        for (int p = 0; p < 4; ++p)
+          st_shared_v4(zs + hh * kTile + swz(r, 4 * h + p), pk[4 * p], pk[4 * p + 1], pk[4 * p + 2],
+                       pk[4 * p + 3]);
+        fence_proxy_async();
+        tc_fence_before();
+        if (l + 1 < L) mbar_arrive(hh == 0 ? z0_ready : z1_ready);
+        if (tr) trace_at(a, l, hh == 0 ? T_EPI_Z0 : T_EPI_Z1, clock64());
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+          *reinterpret_cast<uint4*>(zrow + (size_t)hh * kTile + swz(r, 4 * h + p)) =
               make_uint4(pk[4 * p], pk[4 * p + 1], pk[4 * p + 2], pk[4 * p + 3]);
-        }
       }
-      fence_proxy_async();
-      tc_fence_before();
-      if (l + 1 < L) mbar_arrive(z_ready);
+      par ^= 1;
     }
   }
   tc_fence_before();
@@ -475,7 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(GemmArgs g) {
         const float thr = noise_uniform(prefix, kUniformClass) * total;
         float run = (h == 0) ? 0.f : s0;
         int found = g.A;
-        for (int cc = 0; cc < HALF / 32 && found == g.A; ++cc) {
+        // warp-uniform trip count: tcgen05.ld is .sync.aligned across the warp
+        for (int cc = 0; cc < HALF / 32; ++cc) {
           float v[32];
           tmem_ld32(trow + cbase + 32 * cc, v);
           tmem_wait_ld();
@@ -546,7 +615,7 @@ cudaError_t set_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-constexpr size_t kChainSmem = 1024 + 6 * kTile + kChainStages * kChainStage + 128;
+constexpr size_t kChainSmem = 1024 + 6 * kTile + kChainStages * kChunk + 256;
 
 }  // namespace
 
@@ -559,6 +628,7 @@ bool tc_supported(const CellDims& d, int batch, std::string* why) {
   if (d.R != kR || d.D != kD) return no("needs residual = dilation = 128 channels");
   if (d.S % 128 || d.H % 128 || d.S > 2048 || d.H > 2048) return no("needs skip/head multiples of 128");
   if (d.A != 256) return no("needs 256 classes");
+  if (d.L > kMaxChainLayers) return no("needs at most 128 layers");
   if (batch % 128) return no("needs a batch that is a multiple of 128 streams");
   return true;
 }
@@ -569,20 +639,34 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
   TcState* tc = new TcState();
   h.tc = tc;
   tc->ntile = h.batch / 128;
-  // chain weights: per layer 4 dil chunks of [256 n][64 k] over K = [x_t | x_{t-d}], 2 res chunks
+  auto any_nonzero = [](const float* p, size_t n) {
+    for (size_t i = 0; i < n; ++i)
+      if (p[i] != 0.f) return 1;
+    return 0;
+  };
+  tc->has_dil_bias = any_nonzero(desc->dil_b, (size_t)L * 2 * kD);
+  tc->has_res_bias = any_nonzero(desc->res_b, (size_t)L * kR);
+  // chain weights, per layer in MMA issue order (10 chunks of [128 n][64 k]):
+  //   dil N-half hh in {0,1}, K-chunks 2,3 (x_{t-d}); then per half K-chunks 0,1 (x_t);
+  //   res K-chunks 0,1. N-half hh holds tanh rows 64hh..64hh+63 then sigmoid rows
+  //   D+64hh..D+64hh+63, so one half's accumulator carries both gate inputs.
   {
     std::vector<uint8_t> img((size_t)L * kLayerBytes, 0);
     for (int l = 0; l < L; ++l) {
       uint8_t* base = img.data() + (size_t)l * kLayerBytes;
       const float* w0 = desc->dil_w + ((size_t)l * 2 + 0) * 2 * kD * kR;
       const float* w1 = desc->dil_w + ((size_t)l * 2 + 1) * 2 * kD * kR;
-      for (int c = 0; c < 4; ++c)
-        pack_image(base + c * kDilChunk, 256, c * 64, [&](int n, int k) {
-          return k < kR ? w0[(size_t)n * kR + k] : w1[(size_t)n * kR + (k - kR)];
+      const int order[8][2] = {{0, 2}, {0, 3}, {1, 2}, {1, 3}, {0, 0}, {0, 1}, {1, 0}, {1, 1}};
+      for (int c = 0; c < 8; ++c) {
+        const int hh = order[c][0], kc = order[c][1];
+        pack_image(base + (size_t)c * kChunk, 128, kc * 64, [&](int n, int k) {
+          const int row = n < 64 ? 64 * hh + n : kD + 64 * hh + (n - 64);
+          return k < kR ? w0[(size_t)row * kR + k] : w1[(size_t)row * kR + (k - kR)];
         });
+      }
       const float* wr = desc->res_w + (size_t)l * kR * kD;
       for (int c = 0; c < 2; ++c)
-        pack_image(base + 4 * kDilChunk + c * kResChunk, 128, c * 64,
+        pack_image(base + (size_t)(8 + c) * kChunk, 128, c * 64,
                    [&](int n, int k) { return wr[(size_t)n * kD + k]; });
     }
     if (int rc = upload_bytes(&tc->wchain, img)) return rc;
@@ -652,8 +736,24 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   cudaError_t e = cudaMemcpyAsync(tc->cls, run.inputs, sizeof(int32_t) * B,
                                   cudaMemcpyDeviceToDevice, st);
   if (e != cudaSuccess) return e;
-  ChainArgs ca{B, L, 0, h.d_dil, h.d_qoff, h.d_queue, tc->wchain, h.w.embed, h.w.dil_b,
-               h.w.res_b, tc->cls, tc->zimg};
+  ChainArgs ca{};
+  ca.B = B;
+  ca.L = L;
+  ca.queue = h.d_queue;
+  ca.w = tc->wchain;
+  ca.embed = h.w.embed;
+  ca.dil_b = h.w.dil_b;
+  ca.res_b = h.w.res_b;
+  ca.cls = tc->cls;
+  ca.zimg = tc->zimg;
+  ca.has_dil_bias = tc->has_dil_bias;
+  ca.has_res_bias = tc->has_res_bias;
+  ca.trace = tc->trace;
+  std::vector<int64_t> qoff(L);
+  for (int l = 0, acc = 0; l < L; ++l) {
+    qoff[l] = (int64_t)acc * B * kR;
+    acc += h.dil[l];
+  }
   GemmArgs skip{};
   skip.a = tc->zimg;
   skip.b = tc->wskip;
@@ -681,7 +781,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   h2.cls_next = tc->cls;
   const dim3 gskip(tc->ntile, S / 128), gh1(tc->ntile, H / 128), gh2(tc->ntile, 1);
   for (int i = 0; i < run.n_steps; ++i) {
-    ca.t = run.t0 + i;
+    for (int l = 0; l < L; ++l) ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)B * kR;
     chain_kernel<<<tc->ntile, kThreads, kChainSmem, st>>>(ca);
     gemm_kernel<128, 0><<<gskip, kThreads, gemm_smem<128>(), st>>>(skip);
     gemm_kernel<128, 0><<<gh1, kThreads, gemm_smem<128>(), st>>>(h1);

@@ -87,6 +87,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
 bool tc_supported(const CellDims& d, int batch, std::string* why);
 int tc_create(Handle& h, const fw_cell_desc* desc);
 void tc_destroy(Handle& h);
+void tc_set_trace(Handle& h, long long* trace);
 
 struct PlainDev {
   int n_layers, w, act;

@@ -123,6 +123,27 @@ def test_cfg4_large_batch_bf16(cuda, kernel):
     assert ties <= 4
 
 
+@pytest.mark.parametrize("sampler", [0, 1, 2])
+def test_tcgen05_biases_shapes_and_samplers(cuda, sampler):
+    """Non-zero biases, S != H, 3 layers, every selection rule through the tcgen05 path."""
+    cfg = CellConfig(1, 3, 128, 128, 256, head_channels=384, weight_dtype="bf16",
+                     bias="fan_in", init_seed=7)
+    m = build_cell_model(cfg)
+    B, n = 256, 40
+    gen = CellGenerator(m, B, kernel="tcgen05")
+    assert gen.kernel == "tcgen05"
+    primer = np.random.default_rng(3).integers(0, 256, (3, B))
+    out, lg = run(gen, primer, n, Sampler(sampler, 9), n)
+    ties = check_streams(oc.CellOracle(m, exact=False), primer, out, lg, [0, 77, 255], sampler, 9,
+                         2e-2, 4e-2 if sampler != 1 else 2e-2)
+    assert ties <= 3
+    # the SIMT kernel on the same model agrees with the oracle as well (fp32 math)
+    gen2 = CellGenerator(m, B, kernel="simt")
+    out2, lg2 = run(gen2, primer, n, Sampler(sampler, 9), n)
+    check_streams(oc.CellOracle(m, exact=False), primer, out2, lg2, [0, 255], sampler, 9,
+                  1e-4, 2e-4 if sampler != 1 else 1e-5)
+
+
 def test_cfg5_deep_teacher_forced_walk(cuda):
     spec = configs.cfg5()
     m = build_cell_model(spec.cell)

@@ -1,0 +1,62 @@
+"""Per-layer phase timeline of the tcgen05 chain kernel (CTA 0, clock64 cycles).
+
+    python tools/trace_chain.py [--config cfg4] [--steps 3]
+
+Slots (csrc/cell_tc.cu TraceSlot): MMA thread -- xd_ready seen, xt_ready seen,
+acc0 committed, acc1 committed, z0 seen, z1 seen, x_full committed, cycles
+spent waiting on weight chunks; epilogue thread (warp 2 lane 0) -- xd arrive,
+x_full seen, xt arrive, global traffic issued, acc0 seen, z0 arrive, acc1
+seen, z1 arrive.
+"""
+
+import argparse
+import ctypes as C
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_1611_09482_b200 import CellGenerator, Sampler, _lib, build_cell_model, configs  # noqa: E402
+
+NAMES = ["mma_xd", "mma_xt", "mma_acc0", "mma_acc1", "mma_z0", "mma_z1", "mma_xfull", "mma_wwait",
+         "epi_a", "epi_xfull", "epi_xt", "epi_glob", "epi_acc0", "epi_z0", "epi_acc1", "epi_z1"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="cfg4")
+    ap.add_argument("--steps", type=int, default=3)
+    args = ap.parse_args()
+    spec = configs.by_name(args.config)
+    m = build_cell_model(spec.cell)
+    gen = CellGenerator(m, spec.batch, kernel="tcgen05")
+    L = spec.cell.total_layers
+    tr = torch.zeros((L, 16), dtype=torch.int64, device="cuda")
+    _lib.check(gen._lib.fw_debug_trace(gen._h, C.c_void_p(tr.data_ptr())))
+    primer = torch.full((1, spec.batch), 128, dtype=torch.int32, device="cuda")
+    gen.generate(primer, args.steps, Sampler(spec.sampler, configs.NOISE_SEED))
+    torch.cuda.synchronize()
+    t = tr.cpu().numpy().astype(np.int64)
+    base = t[0, 8]  # epi_a of layer 0
+    print("cycles relative to layer-0 epi_a; per-layer deltas vs that layer's epi_a")
+    print("layer " + " ".join(f"{n:>9s}" for n in NAMES))
+    for l in range(L):
+        row = t[l].copy()
+        ref = row[8]
+        cells = []
+        for i, v in enumerate(row):
+            if i == 7:
+                cells.append(f"{v:9d}")
+            elif v == 0:
+                cells.append(f"{'-':>9s}")
+            else:
+                cells.append(f"{v - ref:9d}")
+        print(f"{l:5d} " + " ".join(cells) + f"   (start {ref - base})")
+    per_layer = np.diff(t[:, 8])
+    print(f"mean cycles/layer {per_layer.mean():.0f}; total {t[-1, 8] - base}; "
+          f"weight-wait cycles total {t[:, 7].sum()}")
+
+
+if __name__ == "__main__":
+    main()
