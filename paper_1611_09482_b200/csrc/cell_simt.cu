@@ -194,12 +194,19 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
 
     for (int l = 0; l < L; ++l) {
       // pop + push on slot t mod d_l: read x_l[t-d], cache x_l[t] (fast.py:192)
+      // slot layout [R/4][B][4] (shared with the tcgen05 path): element (stream s,
+      // channel r) at ((r/4) * B + s) * 4 + r%4; e walks it contiguously per chunk.
       const int dl = p.dil[l];
-      float* q = p.queue + p.qoff[l] + (size_t)(t % dl) * B * R + (size_t)s0 * R;
-      for (int e = tid; e < nb * R; e += NT) {
-        const int b = e / R, r = e % R;
-        const float old = q[e];
-        q[e] = xx[b * 2 * R + r];
+      const int Rp = (R + 3) & ~3;  // channels padded to whole 16-byte chunks
+      float* q = p.queue + p.qoff[l] + (size_t)(t % dl) * B * Rp;
+      for (int e = tid; e < nb * Rp; e += NT) {
+        const int j = e & 3, rest = e >> 2;
+        const int b = rest % nb, c4 = rest / nb;
+        const int r = c4 * 4 + j;
+        if (r >= R) continue;
+        float* slot = q + ((size_t)c4 * B + s0 + b) * 4 + j;
+        const float old = *slot;
+        *slot = xx[b * 2 * R + r];
         xx[b * 2 * R + R + r] = old;
       }
       __syncthreads();

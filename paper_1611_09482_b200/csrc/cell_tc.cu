@@ -105,10 +105,22 @@ __device__ __forceinline__ void ld64(float (&v)[64], const float* p) {
     v[4 * i + 3] = f.w;
   }
 }
-__device__ __forceinline__ void st64(float* p, const float (&v)[64]) {
-  float4* q = reinterpret_cast<float4*>(p);
+// 16 float4 chunks at a stride of `stride` floats (queue layout [R/4][B][4]).
+__device__ __forceinline__ void ld64s(float (&v)[64], const float* p, size_t stride) {
 #pragma unroll
-  for (int i = 0; i < 16; ++i) q[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+  for (int i = 0; i < 16; ++i) {
+    float4 f = *reinterpret_cast<const float4*>(p + i * stride);
+    v[4 * i] = f.x;
+    v[4 * i + 1] = f.y;
+    v[4 * i + 2] = f.z;
+    v[4 * i + 3] = f.w;
+  }
+}
+__device__ __forceinline__ void st64s(float* p, const float (&v)[64], size_t stride) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    *reinterpret_cast<float4*>(p + i * stride) =
+        make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
 }
 // 64 fp32 -> one 128-byte bf16 row of a swizzled [128][64] image
 __device__ __forceinline__ void row_to_image(uint32_t img_saddr, int r, const float (&v)[64]) {
@@ -228,21 +240,29 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
         chunk(tmem + 128, xs + 1 * kTile, false);
         mma_commit(acc1_full);
         trace_at(a, l, T_MMA_ACC1, clock64());
+        // z halves: res MMA (all but the top layer) + TMA bulk store of the z stash
+        uint8_t* zst = a.zimg + ((size_t)tile * L * 2 + 2 * l) * kTile;
+        mbar_wait(z0_ready, par);
+        trace_at(a, l, T_MMA_Z0, clock64());
+        tc_fence_after();
+        bulk_s2g(zst, Z, kTile);
+        if (l + 1 < L) chunk(tmem + 256, zs + 0 * kTile, false);
+        mbar_wait(z1_ready, par);
+        trace_at(a, l, T_MMA_Z1, clock64());
+        tc_fence_after();
+        bulk_s2g(zst + kTile, Z + kTile, kTile);
+        bulk_commit();
+        if (l + 1 < L) chunk(tmem + 256, zs + 1 * kTile, false);
+        // Z is rewritten after x_full: the stash copy must have read it by then
+        bulk_wait_read0();
         if (l + 1 < L) {
-          mbar_wait(z0_ready, par);
-          trace_at(a, l, T_MMA_Z0, clock64());
-          tc_fence_after();
-          chunk(tmem + 256, zs + 0 * kTile, false);
-          mbar_wait(z1_ready, par);
-          trace_at(a, l, T_MMA_Z1, clock64());
-          tc_fence_after();
-          chunk(tmem + 256, zs + 1 * kTile, false);
           mma_commit(x_full);
           trace_at(a, l, T_MMA_XFULL, clock64());
         }
         trace_at(a, l, T_MMA_WWAIT, wwait);
         par ^= 1;
       }
+      bulk_wait0();  // the last layer's stash is globally visible before the kernel ends
     }
     __syncwarp();
   } else {  // ---- epilogue warps 2..9: thread = (row r, half h) ----
@@ -255,10 +275,12 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
     uint32_t par = 0;
     float q[64];
     const bool tr = (warp == 2 && lane == 0);
-    auto qptr = [&](int l) { return a.queue + a.qbase[l] + (size_t)stream * kR + 64 * h; };
+    // queue slot layout [R/4][B][4]: 16-byte chunk j of this thread's 64 channels sits at
+    // ((16h + j) * B + stream) * 4, so a warp's 32 streams touch 512 contiguous bytes.
+    const size_t qstride = (size_t)a.B * 4;
+    auto qptr = [&](int l) { return a.queue + a.qbase[l] + ((size_t)16 * h * a.B + stream) * 4; };
     float* qp = qptr(0);
-    ld64(q, qp);
-    uint8_t* zdst = a.zimg + (size_t)tile * (L * 2) * kTile;
+    ld64s(q, qp, qstride);
     for (int l = 0; l < L; ++l) {
       // (a) x_{t-d} half of the operand: independent of this step's residual stream
       row_to_image(xs + (2 + h) * kTile, r, q);
@@ -299,15 +321,14 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
       mbar_arrive(xt_ready);
       if (tr) trace_at(a, l, T_EPI_XT, clock64());
       // global traffic after the fences so they never wait on it
-      st64(qp, x);  // push the layer input into slot t mod d (read earlier by this thread)
+      st64s(qp, x, qstride);  // push the layer input into slot t mod d (read earlier by this thread)
       if (l + 1 < L) {
         qp = qptr(l + 1);
-        ld64(q, qp);  // prefetch x_{l+1}[t - d_{l+1}]
+        ld64s(q, qp, qstride);  // prefetch x_{l+1}[t - d_{l+1}]
       }
       if (tr) trace_at(a, l, T_EPI_GLOBAL, clock64());
       // (c,d) gate of N-half hh -> z columns 64*hh + [32h, 32h+32)
       const float* bd = a.dil_b + (size_t)l * 2 * kD;
-      uint8_t* zrow = zdst + (size_t)(2 * l) * kTile;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         mbar_wait(hh == 0 ? acc0_full : acc1_full, par);
@@ -338,12 +359,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
                        pk[4 * p + 3]);
         fence_proxy_async();
         tc_fence_before();
-        if (l + 1 < L) mbar_arrive(hh == 0 ? z0_ready : z1_ready);
+        mbar_arrive(hh == 0 ? z0_ready : z1_ready);
         if (tr) trace_at(a, l, hh == 0 ? T_EPI_Z0 : T_EPI_Z1, clock64());
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-          *reinterpret_cast<uint4*>(zrow + (size_t)hh * kTile + swz(r, 4 * h + p)) =
-              make_uint4(pk[4 * p], pk[4 * p + 1], pk[4 * p + 2], pk[4 * p + 3]);
       }
       par ^= 1;
     }
