@@ -55,7 +55,10 @@ namespace {
 using namespace ptx;
 
 constexpr int kThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
-constexpr int kChainStages = 8;
+constexpr int kQueueWarp = 10;  // chain kernel: + warp 10, the queue agent
+constexpr int kChainThreads = 352;
+constexpr int kChainStages = 4;
+constexpr uint32_t kQStage = 65536;  // fp32 staging of one tile's ring slot (128 x 128 x 4 B)
 constexpr uint32_t kChunk = 16384;  // one [128 rows][64] bf16 operand image
 constexpr int kChunksPerLayer = 10;  // 8 dil (2 N-halves x 4 K-chunks) + 2 res
 constexpr uint32_t kLayerBytes = kChunksPerLayer * kChunk;
@@ -144,12 +147,13 @@ __device__ __forceinline__ void row_to_image(uint32_t img_saddr, int r, const fl
 //   [z0_ready] res kc0 ; [z1_ready] res kc1 -> x_full
 // so the x_{t-d} half of the next layer's GEMM overlaps the residual epilogue, and the
 // second N-half overlaps the first half's gate.
-__global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
+__global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* X = smem;                  // 4 chunks
   uint8_t* Z = smem + 4 * kTile;      // 2 chunks
-  uint8_t* ring = smem + 6 * kTile;   // kChainStages x 16 KB
+  uint8_t* Sq = smem + 6 * kTile;     // fp32 queue staging [R/4][128][4] = 64 KB
+  uint8_t* ring = Sq + kQStage;       // kChainStages x 16 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kChainStages * kChunk);
   uint64_t* full = bars;
   uint64_t* empty = bars + kChainStages;
@@ -157,10 +161,12 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
   uint64_t* xt_ready = xd_ready + 1;
   uint64_t* z0_ready = xd_ready + 2;
   uint64_t* z1_ready = xd_ready + 3;
-  uint64_t* acc0_full = xd_ready + 4;
-  uint64_t* acc1_full = xd_ready + 5;
-  uint64_t* x_full = xd_ready + 6;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xd_ready + 7);
+  uint64_t* s_written = xd_ready + 4;
+  uint64_t* acc0_full = xd_ready + 5;
+  uint64_t* acc1_full = xd_ready + 6;
+  uint64_t* x_full = xd_ready + 7;
+  uint64_t* s_full = xd_ready + 8;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xd_ready + 9);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
@@ -171,8 +177,8 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 4; ++i) mbar_init(xd_ready + i, 256);
-    for (int i = 4; i < 7; ++i) mbar_init(xd_ready + i, 1);
+    for (int i = 0; i < 5; ++i) mbar_init(xd_ready + i, 256);
+    for (int i = 5; i < 9; ++i) mbar_init(xd_ready + i, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -181,7 +187,31 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (warp == 0) {
+  if (warp == kQueueWarp) {
+    if (lane == 0) {  // ---- queue agent: HBM ring slot <-> fp32 staging tile, by TMA ----
+      // slot layout [R/4][B][4]: this tile's 16-byte chunk c4 is 2 KB contiguous
+      auto piece = [&](int l, int c4) {
+        return a.queue + a.qbase[l] + ((size_t)c4 * a.B + (size_t)tile * 128) * 4;
+      };
+      auto load_slot = [&](int l) {
+        mbar_arrive_expect_tx(s_full, kQStage);
+        for (int c4 = 0; c4 < kR / 4; ++c4)
+          bulk_g2s(Sq + c4 * 2048, piece(l, c4), 2048, s_full);
+      };
+      load_slot(0);
+      for (int l = 0; l < L; ++l) {
+        mbar_wait(s_written, l & 1);  // epilogue consumed x_{t-d} and wrote x_l into Sq
+        fence_proxy_async();
+        for (int c4 = 0; c4 < kR / 4; ++c4) bulk_s2g(piece(l, c4), Sq + c4 * 2048, 2048);
+        bulk_commit();
+        if (l + 1 < L) {
+          bulk_wait_read0();  // the push has read Sq; reuse it for the next layer's pop
+          load_slot(l + 1);
+        }
+      }
+      bulk_wait0();
+    }
+  } else if (warp == 0) {
     if (lane == 0) {  // ---- weight producer: streams chunks in MMA order ----
       int stage = 0;
       uint32_t phase = 0;
@@ -273,17 +303,19 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
     const uint32_t xs = smem_u32(X), zs = smem_u32(Z);
     const int c = a.cls[stream];
     uint32_t par = 0;
-    float q[64];
     const bool tr = (warp == 2 && lane == 0);
-    // queue slot layout [R/4][B][4]: 16-byte chunk j of this thread's 64 channels sits at
-    // ((16h + j) * B + stream) * 4, so a warp's 32 streams touch 512 contiguous bytes.
-    const size_t qstride = (size_t)a.B * 4;
-    auto qptr = [&](int l) { return a.queue + a.qbase[l] + ((size_t)16 * h * a.B + stream) * 4; };
-    float* qp = qptr(0);
-    ld64s(q, qp, qstride);
+    // staging tile Sq is [R/4][128][4] fp32: this thread's 16-byte chunk j (channels
+    // 64h + 4j ..) of row r sits at ((16h + j) * 128 + r) * 16 -- a warp reads 512
+    // contiguous bytes per chunk, bank-conflict free.
+    float* sq = reinterpret_cast<float*>(Sq) + ((size_t)16 * h * 128 + r) * 4;
     for (int l = 0; l < L; ++l) {
-      // (a) x_{t-d} half of the operand: independent of this step's residual stream
-      row_to_image(xs + (2 + h) * kTile, r, q);
+      // (a) pop: x_{t-d} (staged by the queue agent) -> bf16 half of the operand
+      {
+        mbar_wait(s_full, l & 1);
+        float q[64];
+        ld64s(q, sq, 128 * 4);
+        row_to_image(xs + (2 + h) * kTile, r, q);
+      }
       fence_proxy_async();
       mbar_arrive(xd_ready);
       if (tr) trace_at(a, l, T_EPI_A, clock64());
@@ -320,12 +352,10 @@ __global__ void __launch_bounds__(kThreads, 1) chain_kernel(ChainArgs a) {
       tc_fence_before();
       mbar_arrive(xt_ready);
       if (tr) trace_at(a, l, T_EPI_XT, clock64());
-      // global traffic after the fences so they never wait on it
-      st64s(qp, x, qstride);  // push the layer input into slot t mod d (read earlier by this thread)
-      if (l + 1 < L) {
-        qp = qptr(l + 1);
-        ld64s(q, qp, qstride);  // prefetch x_{l+1}[t - d_{l+1}]
-      }
+      // push: x_l -> staging (same bytes this thread just popped); the agent TMA-stores it
+      st64s(sq, x, 128 * 4);
+      fence_proxy_async();
+      mbar_arrive(s_written);
       if (tr) trace_at(a, l, T_EPI_GLOBAL, clock64());
       // (c,d) gate of N-half hh -> z columns 64*hh + [32h, 32h+32)
       const float* bd = a.dil_b + (size_t)l * 2 * kD;
@@ -632,7 +662,7 @@ cudaError_t set_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-constexpr size_t kChainSmem = 1024 + 6 * kTile + kChainStages * kChunk + 256;
+constexpr size_t kChainSmem = 1024 + 6 * kTile + kQStage + kChainStages * kChunk + 256;
 
 }  // namespace
 
@@ -799,7 +829,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   const dim3 gskip(tc->ntile, S / 128), gh1(tc->ntile, H / 128), gh2(tc->ntile, 1);
   for (int i = 0; i < run.n_steps; ++i) {
     for (int l = 0; l < L; ++l) ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)B * kR;
-    chain_kernel<<<tc->ntile, kThreads, kChainSmem, st>>>(ca);
+    chain_kernel<<<tc->ntile, kChainThreads, kChainSmem, st>>>(ca);
     gemm_kernel<128, 0><<<gskip, kThreads, gemm_smem<128>(), st>>>(skip);
     gemm_kernel<128, 0><<<gh1, kThreads, gemm_smem<128>(), st>>>(h1);
     h2.t = run.t0 + i;
