@@ -55,8 +55,8 @@ namespace {
 using namespace ptx;
 
 constexpr int kThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
-constexpr int kQueueWarp = 10;  // chain kernel: + warp 10, the queue agent
-constexpr int kChainThreads = 352;
+constexpr int kPushWarp0 = 10;  // chain kernel: + warps 10..13 push x_l to the HBM ring
+constexpr int kChainThreads = 448;
 constexpr int kChainStages = 4;
 constexpr uint32_t kQStage = 65536;  // fp32 staging of one tile's ring slot (128 x 128 x 4 B)
 constexpr uint32_t kChunk = 16384;  // one [128 rows][64] bf16 operand image
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
   uint64_t* xt_ready = xd_ready + 1;
   uint64_t* z0_ready = xd_ready + 2;
   uint64_t* z1_ready = xd_ready + 3;
-  uint64_t* s_written = xd_ready + 4;
+  uint64_t* x_read = xd_ready + 4;
   uint64_t* acc0_full = xd_ready + 5;
   uint64_t* acc1_full = xd_ready + 6;
   uint64_t* x_full = xd_ready + 7;
@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 5; ++i) mbar_init(xd_ready + i, 256);
+    for (int i = 0; i < 4; ++i) mbar_init(xd_ready + i, 256);
+    mbar_init(x_read, 128);
     for (int i = 5; i < 9; ++i) mbar_init(xd_ready + i, 1);
     fence_mbar_init();
   }
@@ -187,35 +188,49 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (warp == kQueueWarp) {
-    if (lane == 0) {  // ---- queue agent: HBM ring slot <-> fp32 staging tile, by TMA ----
-      // slot layout [R/4][B][4]: this tile's 16-byte chunk c4 is 2 KB contiguous
-      auto piece = [&](int l, int c4) {
-        return a.queue + a.qbase[l] + ((size_t)c4 * a.B + (size_t)tile * 128) * 4;
-      };
-      auto load_slot = [&](int l) {
-        mbar_arrive_expect_tx(s_full, kQStage);
-        for (int c4 = 0; c4 < kR / 4; ++c4)
-          bulk_g2s(Sq + c4 * 2048, piece(l, c4), 2048, s_full);
-      };
-      load_slot(0);
-      for (int l = 0; l < L; ++l) {
-        mbar_wait(s_written, l & 1);  // epilogue consumed x_{t-d} and wrote x_l into Sq
-        fence_proxy_async();
-        for (int c4 = 0; c4 < kR / 4; ++c4) bulk_s2g(piece(l, c4), Sq + c4 * 2048, 2048);
-        bulk_commit();
-        if (l + 1 < L) {
-          bulk_wait_read0();  // the push has read Sq; reuse it for the next layer's pop
-          load_slot(l + 1);
-        }
+  if (warp >= kPushWarp0) {
+    // ---- push warps 10..13: x_l (TMEM, after the pending bias) -> HBM ring slot t mod d ----
+    const int sub = warp & 3;
+    const int r = sub * 32 + lane;
+    const size_t stream = (size_t)tile * 128 + r;
+    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16) + 256;
+    for (int l = 0; l < L; ++l) {
+      mbar_wait(xt_ready, l & 1);
+      tc_fence_after();
+      // slot layout [R/4][B][4]: a warp's 32 streams write 512 contiguous bytes per chunk
+      float* dst = a.queue + a.qbase[l] + stream * 4;
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        float x[32];
+        tmem_ld32(trow + 32 * q, x);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4*>(dst + (size_t)(8 * q + j) * a.B * 4) =
+              make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
       }
-      bulk_wait0();
+      tc_fence_before();
+      mbar_arrive(x_read);  // the res MMA may now accumulate onto x
     }
   } else if (warp == 0) {
-    if (lane == 0) {  // ---- weight producer: streams chunks in MMA order ----
+    if (lane == 0) {  // ---- weight producer (MMA order) + queue pop prefetch by TMA ----
+      // slot layout [R/4][B][4]: this tile's 16-byte chunk c4 is 2 KB contiguous
+      auto pop = [&](int l) {
+        mbar_arrive_expect_tx(s_full, kQStage);
+        for (int c4 = 0; c4 < kR / 4; ++c4)
+          bulk_g2s(Sq + c4 * 2048, a.queue + a.qbase[l] + ((size_t)c4 * a.B + (size_t)tile * 128) * 4,
+                   2048, s_full);
+      };
+      pop(0);
       int stage = 0;
       uint32_t phase = 0;
       for (int l = 0; l < L; ++l) {
+        if (l > 0) {
+          // Sq is free once every epilogue thread converted layer l-1's x_{t-d}; the slot
+          // of layer l was last written one step ago, so the pop needs no other ordering.
+          mbar_wait(xd_ready, (l - 1) & 1);
+          pop(l);
+        }
         const uint8_t* wl = a.w + (size_t)l * kLayerBytes;
         const int n = (l + 1 < L) ? kChunksPerLayer : 8;
         for (int c = 0; c < n; ++c) {
@@ -264,6 +279,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
         tc_fence_after();
         chunk(tmem + 0, xs + 0 * kTile, false);
         chunk(tmem + 0, xs + 1 * kTile, false);
+        // Z is rewritten once acc0_full is seen: the previous layer's stash copy must have
+        // read it by then
+        bulk_wait_read0();
         mma_commit(acc0_full);
         trace_at(a, l, T_MMA_ACC0, clock64());
         chunk(tmem + 128, xs + 0 * kTile, false);
@@ -276,16 +294,18 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
         trace_at(a, l, T_MMA_Z0, clock64());
         tc_fence_after();
         bulk_s2g(zst, Z, kTile);
-        if (l + 1 < L) chunk(tmem + 256, zs + 0 * kTile, false);
+        if (l + 1 < L) {
+          mbar_wait(x_read, par);  // push warps have read x_l before the MMA updates it
+          tc_fence_after();
+          chunk(tmem + 256, zs + 0 * kTile, false);
+        }
         mbar_wait(z1_ready, par);
         trace_at(a, l, T_MMA_Z1, clock64());
         tc_fence_after();
         bulk_s2g(zst + kTile, Z + kTile, kTile);
         bulk_commit();
-        if (l + 1 < L) chunk(tmem + 256, zs + 1 * kTile, false);
-        // Z is rewritten after x_full: the stash copy must have read it by then
-        bulk_wait_read0();
         if (l + 1 < L) {
+          chunk(tmem + 256, zs + 1 * kTile, false);
           mma_commit(x_full);
           trace_at(a, l, T_MMA_XFULL, clock64());
         }
@@ -352,10 +372,6 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       tc_fence_before();
       mbar_arrive(xt_ready);
       if (tr) trace_at(a, l, T_EPI_XT, clock64());
-      // push: x_l -> staging (same bytes this thread just popped); the agent TMA-stores it
-      st64s(sq, x, 128 * 4);
-      fence_proxy_async();
-      mbar_arrive(s_written);
       if (tr) trace_at(a, l, T_EPI_GLOBAL, clock64());
       // (c,d) gate of N-half hh -> z columns 64*hh + [32h, 32h+32)
       const float* bd = a.dil_b + (size_t)l * 2 * kD;
