@@ -180,13 +180,15 @@ int fw_cell_create(const fw_cell_desc* desc, int32_t batch, int32_t device, int3
     return code;
   };
   const bool bf = desc->weight_dtype == FW_DTYPE_BF16;
-  // queues: layer l holds d_l slots, each [R/4][B][4] fp32 (R padded to a multiple of 4)
+  // queues: layer l holds d_l slots, each [ceil(B/128)][R/4][128][4] fp32 (R padded to a
+  // multiple of 4, streams to a multiple of 128): a 128-stream tile's slot is contiguous
   const int Rp = (R + 3) & ~3;
+  const int64_t Bp = ((int64_t)batch + 127) / 128 * 128;
   std::vector<int64_t> qoff(L);
   int64_t total = 0;
   for (int l = 0; l < L; ++l) {
     qoff[l] = total;
-    total += (int64_t)h.dil[l] * batch * Rp;
+    total += (int64_t)h.dil[l] * Bp * Rp;
   }
   h.queue_elems = total;
   if ((rc = upload(&h.d_dil, h.dil.data(), L))) return fail(rc);

@@ -194,17 +194,20 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
 
     for (int l = 0; l < L; ++l) {
       // pop + push on slot t mod d_l: read x_l[t-d], cache x_l[t] (fast.py:192)
-      // slot layout [R/4][B][4] (shared with the tcgen05 path): element (stream s,
-      // channel r) at ((r/4) * B + s) * 4 + r%4; e walks it contiguously per chunk.
+      // slot layout [ceil(B/128)][R/4][128][4] (shared with the tcgen05 path): element
+      // (stream s, channel r) at ((s/128 * R/4 + r/4) * 128 + s%128) * 4 + r%4; e walks the
+      // tile's streams contiguously per 16-byte channel chunk.
       const int dl = p.dil[l];
       const int Rp = (R + 3) & ~3;  // channels padded to whole 16-byte chunks
-      float* q = p.queue + p.qoff[l] + (size_t)(t % dl) * B * Rp;
+      const size_t slot_elems = (size_t)((B + 127) / 128) * 128 * Rp;
+      float* q = p.queue + p.qoff[l] + (size_t)(t % dl) * slot_elems;
       for (int e = tid; e < nb * Rp; e += NT) {
         const int j = e & 3, rest = e >> 2;
         const int b = rest % nb, c4 = rest / nb;
         const int r = c4 * 4 + j;
         if (r >= R) continue;
-        float* slot = q + ((size_t)c4 * B + s0 + b) * 4 + j;
+        const int s = s0 + b;
+        float* slot = q + ((size_t)((s >> 7) * (Rp / 4) + c4) * 128 + (s & 127)) * 4 + j;
         const float old = *slot;
         *slot = xx[b * 2 * R + r];
         xx[b * 2 * R + R + r] = old;

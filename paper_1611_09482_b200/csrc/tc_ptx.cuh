@@ -14,6 +14,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdint.h>
 
 namespace fw {
@@ -134,10 +135,11 @@ __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t saddr) {
   return d;
 }
 
-// kind::f16 instruction descriptor: bf16 x bf16 -> fp32, both operands K-major.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
+// kind::f16 instruction descriptor: fp16 x fp16 -> fp32 (a/b format 0 = F16, 1 = BF16),
+// both operands K-major (cute::UMMA::InstrDescriptor bit layout).
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, bool bf16 = false) {
+  return (1u << 4) | ((bf16 ? 1u : 0u) << 7) | ((bf16 ? 1u : 0u) << 10) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t idesc,
@@ -147,6 +149,17 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t a, uint64_t b
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+// Same MMA with the A operand in TMEM: lane = row, 32-bit column j holds the bf16 pair
+// (A[r][2j], A[r][2j+1]); one UMMA_K = 16 step is 8 columns (tools/tmem_a_probe.cu).
+__device__ __forceinline__ void mma_bf16_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t b,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
 // Arrives on `bar` once all previously issued MMAs of this thread complete.
@@ -165,6 +178,19 @@ __device__ __forceinline__ float tanh_fast(float x) {
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+// fp16 pair (lo in the low half), round-to-nearest, saturating to the finite range.
+__device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// Both halves of (a, b) through one MUFU op: returns (tanh(a), tanh(b)) at ~fp16 precision.
+__device__ __forceinline__ float2 tanh2_f16(float a, float b) {
+  uint32_t in = pack_h2(a, b), out;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(out) : "r"(in));
+  __half2 h = *reinterpret_cast<__half2*>(&out);
+  return __half22float2(h);
 }
 __device__ __forceinline__ uint32_t swz(int r, int piece) {
   return (uint32_t)((r >> 3) * 1024 + (r & 7) * 128 + ((piece ^ (r & 7)) << 4));
