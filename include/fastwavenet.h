@@ -174,6 +174,10 @@ const char* fw_last_error(void);
  * tcgen05 chain kernel into d_trace [n_layers][16] (NULL disables). Not part
  * of the reference's interface; used by tools/trace_chain.py. */
 int fw_debug_trace(fw_handle* h, int64_t* d_trace);
+/* Diagnostics: copy the first `bytes` of an internal device buffer to d_dst on `stream`.
+ * which = 0: the HBM ring queues (layout in DESIGN.md); tcgen05 handles only: 1 z stash,
+ * 2 ReLU(skip) images, 3 head-hidden images (fp16 operand images). */
+int fw_debug_copy(const fw_handle* h, int32_t which, void* d_dst, int64_t bytes, void* stream);
 /* Library ABI version (major*100 + minor). */
 int32_t fw_version(void);
 

@@ -484,6 +484,25 @@ int fw_debug_trace(fw_handle* fh, int64_t* d_trace) {
   return FW_OK;
 }
 
+int fw_debug_copy(const fw_handle* fh, int32_t which, void* d_dst, int64_t bytes, void* stream) {
+  if (!fh || !d_dst) return invalid("null argument");
+  const Handle& h = fh->h;
+  const void* src = nullptr;
+  int64_t have = 0;
+  if (which == 0) {
+    src = h.is_plain ? (const void*)h.p.queue : (const void*)h.d_queue;
+    have = h.queue_elems * (h.is_plain ? 8 : 4);
+  } else if (!h.is_plain && h.kernel == FW_KERNEL_TCGEN05) {
+    have = tc_debug_buffer(const_cast<Handle&>(h), which, &src);
+  }
+  if (!src) return invalid("unknown buffer selector");
+  if (bytes < 0 || bytes > have) return invalid("byte count exceeds the buffer size");
+  FW_CUDA(cudaSetDevice(h.device));
+  FW_CUDA(cudaMemcpyAsync(d_dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                          static_cast<cudaStream_t>(stream)));
+  return FW_OK;
+}
+
 int fw_step_index(const fw_handle* fh, int64_t* out) {
   if (!fh || !out) return invalid("null argument");
   *out = fh->h.t;

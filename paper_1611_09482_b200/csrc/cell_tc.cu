@@ -50,17 +50,30 @@ void tc_set_trace(Handle& h, long long* trace) {
   if (h.tc) h.tc->trace = trace;
 }
 
+int64_t tc_debug_buffer(Handle& h, int which, const void** src) {
+  TcState* tc = h.tc;
+  if (!tc) return 0;
+  const int64_t tile_bytes = 16384;
+  if (which == 1) {
+    *src = tc->zimg;
+    return (int64_t)tc->ntile * h.dims.L * h.dims.D / 64 * tile_bytes;
+  }
+  if (which == 2) {
+    *src = tc->simg;
+    return (int64_t)tc->ntile * h.dims.S / 64 * tile_bytes;
+  }
+  if (which == 3) {
+    *src = tc->himg;
+    return (int64_t)tc->ntile * h.dims.H / 64 * tile_bytes;
+  }
+  return 0;
+}
+
 namespace {
 
 using namespace ptx;
 
 constexpr int kThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
-constexpr int kPushWarp0 = 10;  // chain kernel: + warps 10..13 push x_l to the HBM ring
-constexpr int kProd2Warp = 14;  // chain kernel: second weight-producer warp
-constexpr int kChainThreads = 480;
-constexpr int kChainStages = 6;
-constexpr uint32_t kXtbCol = 384;  // TMEM columns 384..447: bf16 x_t operand (packed pairs)
-constexpr uint32_t kQStage = 65536;  // fp32 staging of one tile's ring slot (128 x 128 x 4 B)
 constexpr uint32_t kChunk = 16384;  // one [128 rows][64] bf16 operand image
 constexpr int kChunksPerLayer = 10;  // 8 dil (2 N-halves x 4 K-chunks) + 2 res
 constexpr uint32_t kLayerBytes = kChunksPerLayer * kChunk;
@@ -136,300 +149,7 @@ __device__ __forceinline__ void row_to_image(uint32_t img_saddr, int r, const fl
                  pack_h2(v[8 * p + 6], v[8 * p + 7]));
 }
 
-// Chain kernel: one 128-stream tile per CTA, all layers of one step.
-//
-// TMEM columns: acc0 [0,128)  = dil N-half 0 (tanh rows 0..63 | sigmoid rows 0..63)
-//               acc1 [128,256) = dil N-half 1 (tanh rows 64..127 | sigmoid rows 64..127)
-//               x    [256,384) = residual stream x_l (fp32), the res MMA accumulates onto it.
-// Shared: X0,X1 = bf16 x_t (K 0..127), X2,X3 = bf16 x_{t-d} (K 128..255), Z0,Z1 = bf16 z,
-//         8-stage ring of 16 KB weight chunks.
-// Per layer the MMA thread issues, in the producer's streaming order:
-//   [xd_ready] dil h0 kc2,kc3 ; dil h1 kc2,kc3      (x_{t-d} half: independent of x_l)
-//   [xt_ready] dil h0 kc0,kc1 -> acc0_full ; dil h1 kc0,kc1 -> acc1_full
-//   [z0_ready] res kc0 ; [z1_ready] res kc1 -> x_full
-// so the x_{t-d} half of the next layer's GEMM overlaps the residual epilogue, and the
-// second N-half overlaps the first half's gate.
-__global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
-  uint8_t* X = smem;                  // 2 chunks: bf16 x_{t-d} (K 128..255)
-  uint8_t* Z = smem + 2 * kTile;      // 2 chunks
-  uint8_t* Sq = smem + 4 * kTile;     // fp32 queue staging [R/4][128][4] = 64 KB
-  uint8_t* ring = Sq + kQStage;       // kChainStages x 16 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kChainStages * kChunk);
-  uint64_t* full = bars;
-  uint64_t* empty = bars + kChainStages;
-  uint64_t* xd_ready = bars + 2 * kChainStages;
-  uint64_t* xt_ready = xd_ready + 1;
-  uint64_t* z0_ready = xd_ready + 2;
-  uint64_t* z1_ready = xd_ready + 3;
-  uint64_t* x_read = xd_ready + 4;
-  uint64_t* acc0_full = xd_ready + 5;
-  uint64_t* acc1_full = xd_ready + 6;
-  uint64_t* x_full = xd_ready + 7;
-  uint64_t* s_full = xd_ready + 8;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(xd_ready + 9);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
-  const int L = a.L;
-
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kChainStages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    mbar_init(xd_ready, 128);  // arrived by the 4 queue warps
-    for (int i = 1; i < 4; ++i) mbar_init(xd_ready + i, 256);
-    mbar_init(x_read, 128);
-    for (int i = 5; i < 9; ++i) mbar_init(xd_ready + i, 1);
-    fence_mbar_init();
-  }
-  if (warp == 1) tmem_alloc(tmem_holder, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_holder;
-
-  // Queue pop of layer l by TMA: ring slots are laid out [B/128][R/4][128][4], so this
-  // tile's part of the slot is one contiguous 64 KB block -> one bulk copy (bulk-copy cost
-  // is per operation, tools/tma_bw.cu). Issued one layer ahead (written a step ago).
-  auto pop = [&](int l) {
-    mbar_arrive_expect_tx(s_full, kQStage);
-    bulk_g2s(Sq, a.queue + a.qbase[l] + (size_t)tile * (kR / 4) * 512, kQStage, s_full);
-  };
-
-  if (warp >= kPushWarp0 && warp < kPushWarp0 + 4) {
-    // ---- queue warps 10..13, one thread per stream row: per layer
-    //   pop : x_{t-d} staged in Sq by TMA -> fp16 operand chunks X0,X1 (K 128..255)
-    //   push: x_l (TMEM, after the pending bias) -> HBM ring slot t mod d
-    const int sub = warp & 3;
-    const int r = sub * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16) + 256;
-    const uint32_t xs = smem_u32(X);
-    const float* sq = reinterpret_cast<const float*>(Sq) + (size_t)r * 4;
-    for (int l = 0; l < L; ++l) {
-      // pop: Sq holds layer l's slot; X0,X1 are free once layer l-1's dil MMAs are done
-      mbar_wait(s_full, l & 1);
-      if (l > 0) mbar_wait(acc1_full, (l - 1) & 1);
-#pragma unroll 1
-      for (int hx = 0; hx < 2; ++hx) {
-        float q[64];
-        ld64s(q, sq + (size_t)16 * hx * 512, 512);
-        row_to_image(xs + hx * kTile, r, q);
-      }
-      fence_proxy_async();
-      mbar_arrive(xd_ready);
-      // push
-      mbar_wait(xt_ready, l & 1);
-      tc_fence_after();
-      // slot layout [R/4][B][4]: a warp's 32 streams write 512 contiguous bytes per chunk
-      float* dst = a.queue + a.qbase[l] + ((size_t)tile * (kR / 4) * 128 + r) * 4;
-#pragma unroll 1
-      for (int q = 0; q < 4; ++q) {
-        float x[32];
-        tmem_ld32(trow + 32 * q, x);
-        tmem_wait_ld();
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-          *reinterpret_cast<float4*>(dst + (size_t)(8 * q + j) * 512) =
-              make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
-      }
-      tc_fence_before();
-      mbar_arrive(x_read);  // the res MMA may now accumulate onto x
-    }
-  } else if (warp == 0 || warp == kProd2Warp) {
-    if (lane == 0) {
-      // ---- weight producers: two warps alternate chunks (a thread's bulk copies run one
-      // at a time, separate warps overlap), streaming in MMA issue order ----
-      const int p = warp == 0 ? 0 : 1;
-      if (p == 0) pop(0);
-      const int total = kChunksPerLayer * (L - 1) + 8;
-      for (int i = p; i < total; i += 2) {
-        const int l = i / kChunksPerLayer, c = i % kChunksPerLayer;
-        const int stage = i % kChainStages;
-        mbar_wait(&empty[stage], ((i / kChainStages) & 1) ^ 1);
-        mbar_arrive_expect_tx(&full[stage], kChunk);
-        bulk_g2s(ring + stage * kChunk, a.w + (size_t)l * kLayerBytes + (size_t)c * kChunk, kChunk,
-                 &full[stage]);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0) {  // ---- MMA issuer ----
-      int stage = 0;
-      uint32_t phase = 0, par = 0;
-      const uint32_t id = idesc_f16(128, 128);
-      const uint32_t xs = smem_u32(X), zs = smem_u32(Z), rs = smem_u32(ring);
-      long long wwait = 0;
-      // One 64-K weight chunk: A from smem (a_src = shared address) or, for the bf16 x_t
-      // operand, from TMEM (a_src = TMEM column address, 8 columns per UMMA_K).
-      auto chunk = [&](uint32_t d_tmem, uint32_t a_src, bool a_in_tmem, bool first) {
-        const long long w0 = clock64();
-        mbar_wait(&full[stage], phase);
-        wwait += clock64() - w0;
-        tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t bd = sdesc_sw128(rs + stage * kChunk + kk * 32);
-          const uint32_t acc = (first && kk == 0) ? 0u : 1u;
-          if (a_in_tmem)
-            mma_bf16_ta(d_tmem, a_src + kk * 8, bd, id, acc);
-          else
-            mma_bf16(d_tmem, sdesc_sw128(a_src + kk * 32), bd, id, acc);
-        }
-        mma_commit(&empty[stage]);
-        if (++stage == kChainStages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      };
-      const uint32_t xtb = tmem + kXtbCol;
-      for (int l = 0; l < L; ++l) {
-        mbar_wait(xd_ready, par);
-        trace_at(a, l, T_MMA_XD, clock64());
-        if (l + 1 < L) pop(l + 1);  // every epilogue thread has consumed Sq for layer l
-        tc_fence_after();
-        chunk(tmem + 0, xs + 0 * kTile, false, true);
-        chunk(tmem + 0, xs + 1 * kTile, false, false);
-        chunk(tmem + 128, xs + 0 * kTile, false, true);
-        chunk(tmem + 128, xs + 1 * kTile, false, false);
-        mbar_wait(xt_ready, par);
-        trace_at(a, l, T_MMA_XT, clock64());
-        tc_fence_after();
-        chunk(tmem + 0, xtb + 0, true, false);
-        chunk(tmem + 0, xtb + 32, true, false);
-        // Z is rewritten once acc0_full is seen: the previous layer's stash copy must have
-        // read it by then
-        bulk_wait_read0();
-        mma_commit(acc0_full);
-        trace_at(a, l, T_MMA_ACC0, clock64());
-        chunk(tmem + 128, xtb + 0, true, false);
-        chunk(tmem + 128, xtb + 32, true, false);
-        mma_commit(acc1_full);
-        trace_at(a, l, T_MMA_ACC1, clock64());
-        // z halves: res MMA (all but the top layer) + TMA bulk store of the z stash
-        uint8_t* zst = a.zimg + ((size_t)tile * L * 2 + 2 * l) * kTile;
-        mbar_wait(z0_ready, par);
-        trace_at(a, l, T_MMA_Z0, clock64());
-        tc_fence_after();
-        bulk_s2g(zst, Z, kTile);
-        if (l + 1 < L) {
-          mbar_wait(x_read, par);  // push warps have read x_l before the MMA updates it
-          tc_fence_after();
-          chunk(tmem + 256, zs + 0 * kTile, false, false);
-        }
-        mbar_wait(z1_ready, par);
-        trace_at(a, l, T_MMA_Z1, clock64());
-        tc_fence_after();
-        bulk_s2g(zst + kTile, Z + kTile, kTile);
-        bulk_commit();
-        if (l + 1 < L) {
-          chunk(tmem + 256, zs + 1 * kTile, false, false);
-          mma_commit(x_full);
-          trace_at(a, l, T_MMA_XFULL, clock64());
-        }
-        trace_at(a, l, T_MMA_WWAIT, wwait);
-        par ^= 1;
-      }
-      bulk_wait0();  // the last layer's stash is globally visible before the kernel ends
-    }
-    __syncwarp();
-  } else {  // ---- epilogue warps 2..9: thread = (row r, half h) ----
-    const int sub = warp & 3, h = (warp - 2) >> 2;
-    const int r = sub * 32 + lane;
-    const int stream = tile * 128 + r;
-    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
-    const uint32_t zs = smem_u32(Z);
-    const int c = a.cls[stream];
-    uint32_t par = 0;
-    const bool tr = (warp == 2 && lane == 0);
-    for (int l = 0; l < L; ++l) {
-      if (tr) trace_at(a, l, T_EPI_A, clock64());
-      // (b) x_l: embedding at l = 0, else the TMEM residual stream (+ the pending bias)
-      float x[64];
-      if (l == 0) {
-        ld64(x, a.embed + (size_t)c * kR + 64 * h);
-        tmem_st32(trow + 256 + 64 * h, *reinterpret_cast<float(*)[32]>(x));
-        tmem_st32(trow + 256 + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
-      } else {
-        mbar_wait(x_full, par ^ 1);
-        if (tr) trace_at(a, l, T_EPI_XFULL, clock64());
-        tc_fence_after();
-        tmem_ld32(trow + 256 + 64 * h, *reinterpret_cast<float(*)[32]>(x));
-        tmem_ld32(trow + 256 + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
-        tmem_wait_ld();
-        if (a.has_res_bias) {
-          const float4* rb = reinterpret_cast<const float4*>(a.res_b + (size_t)(l - 1) * kR + 64 * h);
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float4 b = __ldg(rb + i);
-            x[4 * i] += b.x;
-            x[4 * i + 1] += b.y;
-            x[4 * i + 2] += b.z;
-            x[4 * i + 3] += b.w;
-          }
-          tmem_st32(trow + 256 + 64 * h, *reinterpret_cast<float(*)[32]>(x));
-          tmem_st32(trow + 256 + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
-        }
-      }
-      {
-        // bf16 x_t operand straight into TMEM (A operand of the x_t MMAs): this thread's
-        // channels 64h..64h+63 are K positions 64h.. -> packed columns 32h..32h+31
-        float pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) pk[i] = __uint_as_float(pack_h2(x[2 * i], x[2 * i + 1]));
-        tmem_st32(trow + kXtbCol + 32 * h, pk);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(xt_ready);
-      if (tr) trace_at(a, l, T_EPI_XT, clock64());
-      if (tr) trace_at(a, l, T_EPI_GLOBAL, clock64());
-      // (c,d) gate of N-half hh -> z columns 64*hh + [32h, 32h+32)
-      const float* bd = a.dil_b + (size_t)l * 2 * kD;
-#pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-        mbar_wait(hh == 0 ? acc0_full : acc1_full, par);
-        if (tr) trace_at(a, l, hh == 0 ? T_EPI_ACC0 : T_EPI_ACC1, clock64());
-        tc_fence_after();
-        float at[32], as[32];
-        tmem_ld32(trow + 128 * hh + 32 * h, at);
-        tmem_ld32(trow + 128 * hh + 64 + 32 * h, as);
-        tmem_wait_ld();
-        if (a.has_dil_bias) {
-          const int j0 = 64 * hh + 32 * h;
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            at[i] += __ldg(bd + j0 + i);
-            as[i] += __ldg(bd + kD + j0 + i);
-          }
-        }
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          // z = tanh(a) * sigmoid(b), sigmoid(b) = 0.5 + 0.5 tanh(b / 2): one f16x2 MUFU op
-          // evaluates both tanh of an element (fp16 precision, the operand precision of z)
-          const float2 t0 = tanh2_f16(at[i], 0.5f * as[i]);
-          const float2 t1 = tanh2_f16(at[i + 1], 0.5f * as[i + 1]);
-          pk[i >> 1] = pack_h2(t0.x * fmaf(0.5f, t0.y, 0.5f), t1.x * fmaf(0.5f, t1.y, 0.5f));
-        }
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-          st_shared_v4(zs + hh * kTile + swz(r, 4 * h + p), pk[4 * p], pk[4 * p + 1], pk[4 * p + 2],
-                       pk[4 * p + 3]);
-        fence_proxy_async();
-        tc_fence_before();
-        mbar_arrive(hh == 0 ? z0_ready : z1_ready);
-        if (tr) trace_at(a, l, hh == 0 ? T_EPI_Z0 : T_EPI_Z1, clock64());
-      }
-      par ^= 1;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 512);
-}
+#include "chain_tc.cuh"
 
 // ---- generic [128 x BN] tile GEMM over pre-swizzled A/B images ----------------------
 struct GemmArgs {
@@ -698,7 +418,6 @@ cudaError_t set_smem(K kernel, size_t bytes) {
   return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 }
 
-constexpr size_t kChainSmem = 1024 + 4 * kTile + kQStage + kChainStages * kChunk + 256;
 
 }  // namespace
 

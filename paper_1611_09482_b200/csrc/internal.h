@@ -88,6 +88,7 @@ bool tc_supported(const CellDims& d, int batch, std::string* why);
 int tc_create(Handle& h, const fw_cell_desc* desc);
 void tc_destroy(Handle& h);
 void tc_set_trace(Handle& h, long long* trace);
+int64_t tc_debug_buffer(Handle& h, int which, const void** src);
 
 struct PlainDev {
   int n_layers, w, act;

@@ -19,15 +19,11 @@ __global__ void stream_kernel(const uint8_t* src, size_t src_bytes, int chunk, i
   }
   __syncthreads();
   // issuer k (threads 0, 32, 64, ...) owns stages [k*stages/issuers, (k+1)*stages/issuers)
-  const int issuers = lane_mode ? blockDim.x / 32 : blockDim.x / 32;
-  int k;
-  if (lane_mode) {
-    if (threadIdx.x >= issuers) return;
-    k = threadIdx.x;
-  } else {
-    if (threadIdx.x % 32 != 0) return;
-    k = threadIdx.x / 32;
-  }
+  // lane_mode = issuing lanes per warp (0 or 1: lane 0 of each warp)
+  const int lpw = lane_mode > 1 ? lane_mode : 1;
+  const int issuers = (blockDim.x / 32) * lpw;
+  if (threadIdx.x % 32 >= lpw) return;
+  const int k = (threadIdx.x / 32) * lpw + threadIdx.x % 32;
   const int my = stages / issuers;
   const long long n = total / chunk / issuers;
   long long t0 = clock64();
@@ -60,12 +56,12 @@ int main(int argc, char** argv) {
   cudaMalloc(&cyc, sizeof(unsigned long long) * ctas);
   const size_t smem = (size_t)stages * chunk + 1024;
   cudaFuncSetAttribute(stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  stream_kernel<<<ctas, 32 * issuers, smem>>>(src, src_bytes, chunk, stages, per_cta, cyc, lane_mode);
+  stream_kernel<<<ctas, 32 * (issuers / (lane_mode > 1 ? lane_mode : 1)), smem>>>(src, src_bytes, chunk, stages, per_cta, cyc, lane_mode);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  stream_kernel<<<ctas, 32 * issuers, smem>>>(src, src_bytes, chunk, stages, per_cta, cyc, lane_mode);
+  stream_kernel<<<ctas, 32 * (issuers / (lane_mode > 1 ? lane_mode : 1)), smem>>>(src, src_bytes, chunk, stages, per_cta, cyc, lane_mode);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
