@@ -88,10 +88,11 @@ constexpr int kMaxChainLayers = 128;
 
 // Device-side phase trace (CTA 0 only, clock64 cycles), enabled by fw_debug_trace.
 // Per layer kTraceSlots entries; see tools/trace_chain.py for the slot meanings.
-constexpr int kTraceSlots = 16;
+constexpr int kTraceSlots = 24;
 enum TraceSlot {
   T_MMA_XD = 0, T_MMA_XT, T_MMA_ACC0, T_MMA_ACC1, T_MMA_Z0, T_MMA_Z1, T_MMA_XFULL, T_MMA_WWAIT,
-  T_EPI_A, T_EPI_XFULL, T_EPI_XT, T_EPI_GLOBAL, T_EPI_ACC0, T_EPI_Z0, T_EPI_ACC1, T_EPI_Z1
+  T_EPI_A, T_EPI_XFULL, T_EPI_XT, T_EPI_GLOBAL, T_EPI_ACC0, T_EPI_Z0, T_EPI_ACC1, T_EPI_Z1,
+  T_Q_XD, T_Q_PUSHED, T_POP0, T_POP1, T_PROD_A, T_PROD_B, T_PROD_C, T_SPARE
 };
 
 struct ChainArgs {

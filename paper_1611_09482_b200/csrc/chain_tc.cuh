@@ -93,13 +93,16 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
         const uint8_t* wl = a.w + (size_t)l * kLayerBytes;  // chunks 0-3 | 4-7 | 8-9
         const uint32_t ph = ((uint32_t)l & 1) ^ 1;
         mbar_wait(emptyA, ph);
+        trace_at(a, l, T_PROD_A, clock64());
         mbar_arrive_expect_tx(fullA, kStageA);
         bulk_g2s(stA, wl, kStageA, fullA);
         mbar_wait(emptyB, ph);
+        trace_at(a, l, T_PROD_B, clock64());
         mbar_arrive_expect_tx(fullB, kStageB);
         bulk_g2s(stB, wl + 4 * kChunk, kStageB, fullB);
         if (l + 1 < L) {
           mbar_wait(emptyC, ph);
+          trace_at(a, l, T_PROD_C, clock64());
           mbar_arrive_expect_tx(fullC, kStageC);
           bulk_g2s(stC, wl + 8 * kChunk, kStageC, fullC);
         }
@@ -110,6 +113,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       for (int k = 0; k < 2 * L; ++k) {
         const int l = k >> 1, h = k & 1;
         if (k > 0) mbar_wait(sq_free, (uint32_t)(k - 1) & 1);
+        trace_at(a, l, h ? T_POP1 : T_POP0, clock64());
         mbar_arrive_expect_tx(s_full, kSqBytes);
         bulk_g2s(Sq, a.queue + a.qbase[l] + ((size_t)tile * (kR / 4) + 16 * h) * 512, kSqBytes,
                  s_full);
@@ -138,18 +142,29 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
         for (int kk = 0; kk < 4; ++kk)
           mma_bf16(d, sdesc_sw128(a_saddr + kk * 32), sdesc_sw128(b_saddr + kk * 32), id, 1u);
       };
-      for (int l = 0; l < L; ++l) {
-        const uint32_t par = (uint32_t)l & 1;
-        // x_{t-d} half: stage A chunks [h0 kc2, h0 kc3, h1 kc2, h1 kc3]
-        mbar_wait(xd_ready, par);
-        trace_at(a, l, T_MMA_XD, clock64());
-        tc_fence_after();
-        wait_w(fullA, par);
+      // x_{t-d} half, stage A chunks [h0 kc2, h0 kc3 | h1 kc2, h1 kc3]. N-half 0 initialises
+      // acc0 and is issued as early as its operands allow (during the previous layer's
+      // second gate half, when the tensor pipe idles); N-half 1 follows the critical acc0.
+      auto xd_h0 = [&](int l) {
         mma_tmem_a(tmem + 0, tmem + kColXd + 0, sa + 0 * kChunk, true);
         mma_tmem_a(tmem + 0, tmem + kColXd + 32, sa + 1 * kChunk, false);
+      };
+      auto xd_h1 = [&]() {
         mma_tmem_a(tmem + 128, tmem + kColXd + 0, sa + 2 * kChunk, true);
         mma_tmem_a(tmem + 128, tmem + kColXd + 32, sa + 3 * kChunk, false);
         mma_commit(emptyA);
+      };
+      bool h0_early = false;
+      for (int l = 0; l < L; ++l) {
+        const uint32_t par = (uint32_t)l & 1;
+        if (!h0_early) {
+          mbar_wait(xd_ready, par);
+          tc_fence_after();
+          wait_w(fullA, par);
+          xd_h0(l);
+        }
+        trace_at(a, l, T_MMA_XD, clock64());
+        h0_early = false;
         // x_t half: stage B chunks [h0 kc0, h0 kc1, h1 kc0, h1 kc1]
         mbar_wait(xt_ready, par);
         trace_at(a, l, T_MMA_XT, clock64());
@@ -160,6 +175,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
         bulk_wait_read0();  // Z is rewritten once acc0_full is seen: stash copy done reading
         mma_commit(acc0_full);
         trace_at(a, l, T_MMA_ACC0, clock64());
+        xd_h1();
         mma_tmem_a(tmem + 128, tmem + kColXt + 0, sb + 2 * kChunk, false);
         mma_tmem_a(tmem + 128, tmem + kColXt + 32, sb + 3 * kChunk, false);
         mma_commit(acc1_full);
@@ -174,6 +190,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
           tc_fence_after();
           wait_w(fullC, par);
           mma_smem_a(tmem + 256, zs + 0 * kTile, sc + 0 * kChunk);
+          // acc0 is free (gate half 0 done): start layer l+1's x_{t-d} N-half 0 now if its
+          // operand and weights are already in place -- never wait for them here
+          const uint32_t pn = (uint32_t)(l + 1) & 1;
+          if (mbar_test(xd_ready, pn) && mbar_test(fullA, pn)) {
+            tc_fence_after();
+            xd_h0(l + 1);
+            h0_early = true;
+          }
         }
         mbar_wait(z1_ready, par);
         trace_at(a, l, T_MMA_Z1, clock64());
@@ -198,26 +222,41 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
     const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
     const float* sq = reinterpret_cast<const float*>(Sq) + (size_t)r * 4;
     for (int l = 0; l < L; ++l) {
-      // pop: x_l[t-d] from Sq (two halves) -> fp16 -> TMEM xd; the xd columns are free once
-      // layer l-1's dil MMAs are done
-      if (l > 0) mbar_wait(acc1_full, (uint32_t)(l - 1) & 1);
-#pragma unroll 1
+      // pop: x_l[t-d] from Sq (two halves) -> packed fp16 in registers, releasing Sq as soon
+      // as a half is consumed so the next half's copy starts at once; then, once layer l-1's
+      // dil MMAs are done with the xd columns, -> TMEM xd
+      uint32_t pk[2][32];
+#pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int k = 2 * l + h;
         mbar_wait(s_full, (uint32_t)k & 1);
-        float q[64];
-        ld64s(q, sq, 512);  // Sq is [16][128][4]: chunk j of row r at (j * 128 + r) * 16 B
-        float pk[32];
+        const float* src = sq;  // Sq is [16][128][4]: chunk j of row r at (j * 128 + r) * 16 B
 #pragma unroll
-        for (int i = 0; i < 32; ++i) pk[i] = __uint_as_float(pack_h2(q[2 * i], q[2 * i + 1]));
-        tmem_st32(trow + kColXd + 32 * h, pk);
-        // release Sq only after every shared load has returned: the TMEM store consumes
-        // all of them and wait::st retires it. The next pop overwrites Sq via the async proxy.
-        tmem_wait_st();
+        for (int j = 0; j < 16; ++j) {
+          const float4 f = *reinterpret_cast<const float4*>(src + (size_t)j * 512);
+          pk[h][2 * j] = pack_h2(f.x, f.y);
+          pk[h][2 * j + 1] = pack_h2(f.z, f.w);
+        }
+        // every shared load must have returned before Sq is released (the next pop
+        // overwrites it through the async proxy): make the arrive depend on all of them
+        asm volatile("" ::"r"(pk[h][0] ^ pk[h][1] ^ pk[h][2] ^ pk[h][3] ^ pk[h][4] ^ pk[h][5] ^
+                               pk[h][6] ^ pk[h][7] ^ pk[h][8] ^ pk[h][9] ^ pk[h][10] ^ pk[h][11] ^
+                               pk[h][12] ^ pk[h][13] ^ pk[h][14] ^ pk[h][15] ^ pk[h][16] ^
+                               pk[h][17] ^ pk[h][18] ^ pk[h][19] ^ pk[h][20] ^ pk[h][21] ^
+                               pk[h][22] ^ pk[h][23] ^ pk[h][24] ^ pk[h][25] ^ pk[h][26] ^
+                               pk[h][27] ^ pk[h][28] ^ pk[h][29] ^ pk[h][30] ^ pk[h][31])
+                     : "memory");
+        // generic-proxy reads of Sq must be ordered before the async-proxy (TMA) overwrite
+        fence_proxy_async();
         mbar_arrive(sq_free);
       }
+      if (l > 0) mbar_wait(acc1_full, (uint32_t)(l - 1) & 1);
+      tmem_st32(trow + kColXd, *reinterpret_cast<float(*)[32]>(pk[0]));
+      tmem_st32(trow + kColXd + 32, *reinterpret_cast<float(*)[32]>(pk[1]));
+      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(xd_ready);
+      if (warp == kQueueWarp0 && lane == 0) trace_at(a, l, T_Q_XD, clock64());
       // push: x_l (after the pending bias) -> ring slot t mod d_l, 512 B per warp store
       mbar_wait(xt_ready, (uint32_t)l & 1);
       tc_fence_after();
@@ -234,6 +273,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       }
       tc_fence_before();
       mbar_arrive(x_read);
+      if (warp == kQueueWarp0 && lane == 0) trace_at(a, l, T_Q_PUSHED, clock64());
     }
   } else if (warp >= 2 && warp < 10) {
     // ---- gate warps: (row r, column half h) ----
@@ -305,13 +345,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
         }
         uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          // z = tanh(a) * sigmoid(b), sigmoid(b) = 0.5 + 0.5 tanh(b / 2): one f16x2 MUFU op
-          // evaluates both tanh of an element (fp16 precision, the operand precision of z)
-          const float2 t0 = tanh2_f16(at[i], 0.5f * as[i]);
-          const float2 t1 = tanh2_f16(at[i + 1], 0.5f * as[i + 1]);
-          pk[i >> 1] = pack_h2(t0.x * fmaf(0.5f, t0.y, 0.5f), t1.x * fmaf(0.5f, t1.y, 0.5f));
-        }
+        for (int i = 0; i < 32; i += 2)
+          // z = tanh(a) * sigmoid(b) with sigmoid(b) = 0.5 + 0.5 tanh(b / 2), evaluated for
+          // an element pair in packed fp16 (z's operand precision): 2 MUFU + 2 HFMA2 per pair
+          pk[i >> 1] = gate2_h2(at[i], at[i + 1], as[i], as[i + 1]);
 #pragma unroll
         for (int p = 0; p < 4; ++p)
           st_shared_v4(zs + hh * kTile + swz(r, 4 * h + p), pk[4 * p], pk[4 * p + 1], pk[4 * p + 2],

@@ -52,6 +52,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Non-blocking probe: has the phase with this parity completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t done;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(done)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return done != 0;
+}
+
 // Global -> shared bulk copy completing on an mbarrier (TMA engine, UBLKCP).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -185,6 +198,19 @@ __device__ __forceinline__ uint32_t pack_h2(float lo, float hi) {
   asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// Gated unit for an element pair in packed fp16: z = tanh(a) * (0.5 + 0.5 tanh(b / 2)),
+// returned as the packed fp16 pair (z0, z1) -- the operand format z is consumed in.
+__device__ __forceinline__ uint32_t gate2_h2(float a0, float a1, float b0, float b1) {
+  const uint32_t ta_in = pack_h2(a0, a1), tb_in = pack_h2(0.5f * b0, 0.5f * b1);
+  uint32_t ta, tb, z;
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(ta) : "r"(ta_in));
+  asm("tanh.approx.f16x2 %0, %1;" : "=r"(tb) : "r"(tb_in));
+  const uint32_t half2_half = 0x38003800u;  // (0.5, 0.5)
+  asm("fma.rn.f16x2 %0, %1, %2, %2;" : "=r"(tb) : "r"(tb), "r"(half2_half));
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(z) : "r"(ta), "r"(tb));
+  return z;
+}
+
 // Both halves of (a, b) through one MUFU op: returns (tanh(a), tanh(b)) at ~fp16 precision.
 __device__ __forceinline__ float2 tanh2_f16(float a, float b) {
   uint32_t in = pack_h2(a, b), out;

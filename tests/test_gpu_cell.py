@@ -144,6 +144,25 @@ def test_tcgen05_biases_shapes_and_samplers(cuda, sampler):
                   1e-4, 2e-4 if sampler != 1 else 1e-5)
 
 
+def test_tcgen05_matches_simt_all_streams_many_steps(cuda):
+    """Race detector: every stream of cfg4, 32 teacher-forced steps, tcgen05 vs the fp32 SIMT
+    kernel. The chain kernel overlaps TMA, tensor-core and epilogue work with mbarriers; a
+    missing ordering edge shows up as a whole tile (or a few rows) drifting after a few
+    steps, which the 4-stream oracle checks above can miss."""
+    spec = configs.cfg4()
+    m = build_cell_model(spec.cell)
+    n = 32
+    cls = np.random.default_rng(11).integers(0, 256, (n, spec.batch)).astype(np.int32)
+    lg = {}
+    for k in ("tcgen05", "simt"):
+        g = CellGenerator(m, spec.batch, kernel=k)
+        _, l = run(g, cls, n, Sampler(0), n)
+        lg[k] = l
+        g.close()
+    dev = np.abs(lg["tcgen05"] - lg["simt"]).max(axis=2)
+    assert dev.max() <= 2e-2, (dev.max(), np.argwhere(dev > 2e-2)[:8].tolist())
+
+
 def test_cfg5_deep_teacher_forced_walk(cuda):
     spec = configs.cfg5()
     m = build_cell_model(spec.cell)

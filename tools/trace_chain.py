@@ -20,7 +20,9 @@ sys.path.insert(0, ".")
 from paper_1611_09482_b200 import CellGenerator, Sampler, _lib, build_cell_model, configs  # noqa: E402
 
 NAMES = ["mma_xd", "mma_xt", "mma_acc0", "mma_acc1", "mma_z0", "mma_z1", "mma_xfull", "mma_wwait",
-         "epi_a", "epi_xfull", "epi_xt", "epi_glob", "epi_acc0", "epi_z0", "epi_acc1", "epi_z1"]
+         "epi_a", "epi_xfull", "epi_xt", "epi_glob", "epi_acc0", "epi_z0", "epi_acc1", "epi_z1",
+         "q_xd", "q_pushed", "pop0", "pop1", "prod_a", "prod_b", "prod_c", "spare"]
+SLOTS = len(NAMES)
 
 
 def main():
@@ -32,7 +34,7 @@ def main():
     m = build_cell_model(spec.cell)
     gen = CellGenerator(m, spec.batch, kernel="tcgen05")
     L = spec.cell.total_layers
-    tr = torch.zeros((L, 16), dtype=torch.int64, device="cuda")
+    tr = torch.zeros((L, SLOTS), dtype=torch.int64, device="cuda")
     _lib.check(gen._lib.fw_debug_trace(gen._h, C.c_void_p(tr.data_ptr())))
     primer = torch.full((1, spec.batch), 128, dtype=torch.int32, device="cuda")
     gen.generate(primer, args.steps, Sampler(spec.sampler, configs.NOISE_SEED))
@@ -40,18 +42,18 @@ def main():
     t = tr.cpu().numpy().astype(np.int64)
     base = t[0, 8]  # epi_a of layer 0
     print("cycles relative to layer-0 epi_a; per-layer deltas vs that layer's epi_a")
-    print("layer " + " ".join(f"{n:>9s}" for n in NAMES))
+    print("layer " + " ".join(f"{n[:8]:>8s}" for n in NAMES))
     for l in range(L):
         row = t[l].copy()
         ref = row[8]
         cells = []
         for i, v in enumerate(row):
             if i == 7:
-                cells.append(f"{v:9d}")
+                cells.append(f"{v:8d}")
             elif v == 0:
-                cells.append(f"{'-':>9s}")
+                cells.append(f"{'-':>8s}")
             else:
-                cells.append(f"{v - ref:9d}")
+                cells.append(f"{v - ref:8d}")
         print(f"{l:5d} " + " ".join(cells) + f"   (start {ref - base})")
     per_layer = np.diff(t[:, 8])
     print(f"mean cycles/layer {per_layer.mean():.0f}; total {t[-1, 8] - base}; "
