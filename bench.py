@@ -172,6 +172,7 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="override total streams")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--sampler", type=int, default=-1, help="override the config's selection rule")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -227,7 +228,7 @@ def main():
     offset = rank * B
     model = build_cell_model(spec.cell)
     gen = CellGenerator(model, B, kernel=args.kernel)
-    sampler = Sampler(spec.sampler, configs.NOISE_SEED, offset)
+    sampler = Sampler(spec.sampler if args.sampler < 0 else args.sampler, configs.NOISE_SEED, offset)
     primer = torch.full((1, B), spec.primer_class, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 

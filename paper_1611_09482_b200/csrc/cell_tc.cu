@@ -171,13 +171,19 @@ struct GemmArgs {
   int64_t t;
 };
 
+// Each pipeline stage holds kGemmGroup consecutive 64-K chunks of A and of B, each side
+// fetched by ONE bulk copy (consecutive chunks are contiguous in the images) from its own
+// producer warp: copy cost is per operation and a thread's copies run one at a time
+// (tools/ring_bw.cu), so fewer, larger copies from two warps keep the tensor pipe fed.
+constexpr int kGemmGroup = 2;
+constexpr int kGemmThreads = 352;  // warp 0: A producer, 1: MMA, 2..9: epilogue, 10: B producer
 template <int BN>
 constexpr int gemm_stages() {
-  return BN == 256 ? 3 : 4;
+  return BN == 256 ? 2 : 3;
 }
 template <int BN>
 constexpr uint32_t gemm_stage_bytes() {
-  return kTile + BN * 128;
+  return kGemmGroup * (kTile + BN * 128);
 }
 template <int BN>
 constexpr size_t gemm_smem() {
@@ -190,11 +196,12 @@ __device__ __forceinline__ float gumbel_score(float v, uint32_t prefix, int cls)
 }
 
 template <int BN, int EPI>
-__global__ void __launch_bounds__(kThreads, 1) gemm_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   constexpr int S = gemm_stages<BN>();
   constexpr uint32_t SB = gemm_stage_bytes<BN>();
+  constexpr uint32_t A_BYTES = kGemmGroup * kTile, B_BYTES = kGemmGroup * BN * 128;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * SB);
   uint64_t* full = bars;
   uint64_t* empty = bars + S;
@@ -203,9 +210,10 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(GemmArgs g) {
   float* xch = reinterpret_cast<float*>(smem + S * SB + 256);  // [4][128][2] exchange
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = blockIdx.x, nt = blockIdx.y;
+  const int groups = g.kch / kGemmGroup;
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], 2);  // one expect_tx arrival per producer warp
       mbar_init(&empty[i], 1);
     }
     mbar_init(acc_full, 1);
@@ -217,41 +225,36 @@ __global__ void __launch_bounds__(kThreads, 1) gemm_kernel(GemmArgs g) {
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 10) {
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      const uint8_t* abase = g.a + (size_t)mt * g.kch * kTile;
-      const uint8_t* bbase = g.b + (size_t)nt * g.kch * (BN * 128);
-      for (int kc = 0; kc < g.kch; ++kc) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], SB);
-        bulk_g2s(smem + stage * SB, abase + (size_t)kc * kTile, kTile, &full[stage]);
-        bulk_g2s(smem + stage * SB + kTile, bbase + (size_t)kc * (BN * 128), BN * 128, &full[stage]);
-        if (++stage == S) {
-          stage = 0;
-          phase ^= 1;
-        }
+      const bool is_a = warp == 0;
+      const uint8_t* base = is_a ? g.a + (size_t)mt * g.kch * kTile
+                                 : g.b + (size_t)nt * g.kch * (BN * 128);
+      const uint32_t bytes = is_a ? A_BYTES : B_BYTES;
+      for (int gi = 0; gi < groups; ++gi) {
+        const int stage = gi % S;
+        mbar_wait(&empty[stage], ((uint32_t)(gi / S) & 1) ^ 1);
+        mbar_arrive_expect_tx(&full[stage], bytes);
+        bulk_g2s(smem + stage * SB + (is_a ? 0 : A_BYTES), base + (size_t)gi * bytes, bytes,
+                 &full[stage]);
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
       const uint32_t id = idesc_f16(128, BN);
       const uint32_t s0 = smem_u32(smem);
-      for (int kc = 0; kc < g.kch; ++kc) {
-        mbar_wait(&full[stage], phase);
+      for (int gi = 0; gi < groups; ++gi) {
+        const int stage = gi % S;
+        mbar_wait(&full[stage], (uint32_t)(gi / S) & 1);
         tc_fence_after();
+        const uint32_t sa = s0 + stage * SB, sb = sa + A_BYTES;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          mma_bf16(tmem, sdesc_sw128(s0 + stage * SB + kk * 32),
-                   sdesc_sw128(s0 + stage * SB + kTile + kk * 32), id, (kc | kk) != 0);
+        for (int c = 0; c < kGemmGroup; ++c)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16(tmem, sdesc_sw128(sa + c * kTile + kk * 32),
+                     sdesc_sw128(sb + c * (BN * 128) + kk * 32), id, (gi | c | kk) != 0);
         mma_commit(&empty[stage]);
-        if (++stage == S) {
-          stage = 0;
-          phase ^= 1;
-        }
       }
       mma_commit(acc_full);
     }
@@ -586,13 +589,13 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   for (int i = 0; i < run.n_steps; ++i) {
     for (int l = 0; l < L; ++l) ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)B * kR;
     chain_kernel<<<tc->ntile, kChainThreads, kChainSmem, st>>>(ca);
-    gemm_kernel<128, 0><<<gskip, kThreads, gemm_smem<128>(), st>>>(skip);
-    gemm_kernel<128, 0><<<gh1, kThreads, gemm_smem<128>(), st>>>(h1);
+    gemm_kernel<128, 0><<<gskip, kGemmThreads, gemm_smem<128>(), st>>>(skip);
+    gemm_kernel<128, 0><<<gh1, kGemmThreads, gemm_smem<128>(), st>>>(h1);
     h2.t = run.t0 + i;
     h2.logits = (run.logits && i < run.n_logit_steps) ? run.logits + (size_t)i * B * d.A : nullptr;
     h2.out_cls = run.out + (size_t)i * B;
     h2.next_inputs = (i + 1 < run.n_inputs) ? run.inputs + (size_t)(i + 1) * B : nullptr;
-    gemm_kernel<256, 1><<<gh2, kThreads, gemm_smem<256>(), st>>>(h2);
+    gemm_kernel<256, 1><<<gh2, kGemmThreads, gemm_smem<256>(), st>>>(h2);
   }
   *launches = 4 * (int64_t)run.n_steps;
   return cudaGetLastError();
