@@ -121,16 +121,33 @@ def step_accounting(cell, batch):
     return flops, weight_bytes + queue_bytes + io_bytes, queue_bytes
 
 
-def traffic_per_step(config_name, kernel):
-    """DRAM bytes per step from the committed ncu --set full summary, if any."""
+def dominant_accounting(cell, batch, kernel):
+    """Algorithmic FLOPs and bytes per step of the dominant kernel.
+
+    tcgen05: the chain kernel -- the dilated-conv and residual projections of every layer
+    (the skip/head GEMMs run in separate launches), the chain weights once, and one queue
+    slot read + written per layer per stream. SIMT: the whole step."""
+    if kernel != "tcgen05":
+        f, b, _ = step_accounting(cell, batch)
+        return f, b
+    L, R, D = cell.total_layers, cell.residual_channels, cell.dilation_channels
+    macs = L * 4 * D * R + (L - 1) * R * D
+    wbytes = 2 * (L * (4 * D * R + R * D))
+    qbytes = batch * L * 2 * R * 4
+    return 2 * macs * batch, wbytes + qbytes + batch * R * 4
+
+
+def traffic_per_launch(kernel):
+    """DRAM bytes of one dominant-kernel launch from the newest committed ncu summary."""
+    want = "chain_kernel" if kernel == "tcgen05" else "cell_simt_kernel"
     for f in sorted((ROOT / "profiles").glob("ncu_summary_*.json"), reverse=True):
         try:
             d = json.loads(f.read_text())
         except ValueError:
             continue
-        key = f"{config_name}/{kernel}"
-        if key in d and d[key].get("dram_bytes_per_step"):
-            return d[key]["dram_bytes_per_step"], f.name
+        for k in d.get("kernels", []):
+            if want in k.get("kernel", "") and k.get("dram_read") is not None:
+                return k["dram_read"] + k["dram_write"], f.name
     return None, None
 
 
@@ -221,11 +238,10 @@ def main():
     torch.cuda.set_device(dev)
 
     from paper_1611_09482_b200 import CellGenerator, Sampler
+    from paper_1611_09482_b200.distributed import gather_sequences, shard_streams
 
-    if total_batch % world:
-        raise SystemExit("batch must divide over the ranks")
-    B = total_batch // world
-    offset = rank * B
+    shard = shard_streams(total_batch, world, rank)
+    B, offset = shard.count, shard.offset
     model = build_cell_model(spec.cell)
     gen = CellGenerator(model, B, kernel=args.kernel)
     sampler = Sampler(spec.sampler if args.sampler < 0 else args.sampler, configs.NOISE_SEED, offset)
@@ -261,8 +277,8 @@ def main():
 
     # end-to-end through the public host-buffer API (copies inside the timed region)
     gen.reset()
-    host_in = np.full((1, B), spec.primer_class, dtype=np.int32)
-    host_out = np.empty((args.steps, B), dtype=np.int32)
+    host_in = torch.full((1, B), spec.primer_class, dtype=torch.int32).pin_memory().numpy()
+    host_out = torch.empty((args.steps, B), dtype=torch.int32).pin_memory().numpy()
     gen.generate_host(host_in, 1, sampler, out=host_out[:1])  # warm the host path
     gen.reset()
     barrier()
@@ -277,14 +293,25 @@ def main():
         e2e_s = float(t.item())
     same = bool(np.array_equal(host_out, out.cpu().numpy()))
 
+    # dominant-kernel time per step, CUDA events on the launching stream (separate pass so
+    # the timed region above carries no extra events)
+    gen.reset()
+    gen.set_kernel_timing(True)
+    nk = min(args.steps, 100)
+    gen.generate(primer, nk, sampler)
+    torch.cuda.synchronize()
+    k_ms, _, k_steps = gen.kernel_times()
+    gen.set_kernel_timing(False)
+    kernel_s_per_step = k_ms / 1e3 / max(k_steps, 1)
+
     # final gather of the generated sequences (the only collective)
     gather_ms = None
     if world > 1:
         g0 = time.perf_counter()
-        full = torch.empty((world, args.steps, B), dtype=torch.int32, device=dev)
-        torch.distributed.all_gather_into_tensor(full, out)
+        full = gather_sequences(out, shard, total_batch)
         torch.cuda.synchronize()
         gather_ms = 1e3 * (time.perf_counter() - g0)
+        assert full.shape == (args.steps, total_batch)
 
     if rank == 0:
         peaks = load_peaks()
@@ -299,24 +326,32 @@ def main():
         t_flop = per_gpu_flops / comp_peak
         t_byte = per_gpu_bytes / hbm
         kname = gen.kernel
-        traffic, tsrc = traffic_per_step(spec.name, kname)
-        if t_flop >= t_byte:
+        # dominant kernel: the tcgen05 chain kernel (one launch per step) or the SIMT
+        # kernel (one launch per generate call, all of the step's work)
+        k_flops, k_bytes = dominant_accounting(spec.cell, B, kname)
+        k_s = kernel_s_per_step
+        kt_flop, kt_byte = k_flops / comp_peak, k_bytes / hbm
+        if kt_flop >= kt_byte:
             roof = {"bound": "tensor" if spec.cell.weight_dtype == "bf16" else "fp32",
-                    "achieved": per_gpu_flops / s_per_step / 1e12, "peak": comp_peak / 1e12,
+                    "achieved": k_flops / k_s / 1e12, "peak": comp_peak / 1e12,
                     "unit": "TFLOP/s"}
         else:
-            roof = {"bound": "hbm", "achieved": per_gpu_bytes / s_per_step / 1e9,
-                    "peak": hbm / 1e9, "unit": "GB/s"}
+            roof = {"bound": "hbm", "achieved": k_bytes / k_s / 1e9, "peak": hbm / 1e9,
+                    "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        roof["traffic"] = traffic * args.steps if traffic else None
-        roof["traffic_unit"] = "bytes per launch (K steps)"
+        traffic, tsrc = traffic_per_launch(kname)
+        roof["traffic"] = traffic
+        roof["kernel"] = ("chain_kernel (one launch per step)" if kname == "tcgen05"
+                          else "cell_simt_kernel (one launch per generate call, per-step share)")
+        roof["algorithmic_per_step"] = {"flop": k_flops, "bytes": k_bytes}
+        roof["kernel_us_per_step"] = 1e6 * k_s
+        roof["kernel_share_of_step"] = k_s / s_per_step
         roof["step_roofline_us"] = 1e6 * max(t_flop, t_byte)
         roof["step_roofline_frac"] = max(t_flop, t_byte) / s_per_step
-        roof["kernel"] = f"cell_{kname} (one persistent launch per generate call)"
         roof["peak_source"] = peaks["source"] + (
             ", bf16 sustained" if spec.cell.weight_dtype == "bf16" else ", fp32 = 148x128x2x1.965GHz (computed)")
         if tsrc:
-            roof["traffic_source"] = f"profiles/{tsrc}"
+            roof["traffic_source"] = f"profiles/{tsrc} (ncu --set full, one launch)"
         line = {
             "metric": metric, "value": value, "unit": "samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,

@@ -178,6 +178,11 @@ int fw_debug_trace(fw_handle* h, int64_t* d_trace);
  * which = 0: the HBM ring queues (layout in DESIGN.md); tcgen05 handles only: 1 z stash,
  * 2 ReLU(skip) images, 3 head-hidden images (fp16 operand images). */
 int fw_debug_copy(const fw_handle* h, int32_t which, void* d_dst, int64_t bytes, void* stream);
+/* Diagnostics: when enabled, cell generate calls record CUDA events around each step's
+ * dominant (chain) kernel and the whole step, on the caller's stream. _read synchronises
+ * and returns the summed milliseconds and the number of steps covered (up to 1,024). */
+int fw_debug_timing(fw_handle* h, int32_t enable);
+int fw_debug_timing_read(fw_handle* h, double* chain_ms, double* step_ms, int64_t* steps);
 /* Library ABI version (major*100 + minor). */
 int32_t fw_version(void);
 

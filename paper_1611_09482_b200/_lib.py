@@ -21,7 +21,7 @@ EXPORTS = (
     "fw_plain_create", "fw_plain_step", "fw_plain_generate", "fw_plain_pop",
     "fw_plain_compute", "fw_plain_push", "fw_reset", "fw_step_index", "fw_queue_bytes",
     "fw_kernel_kind", "fw_last_launch_count", "fw_destroy", "fw_last_error", "fw_version",
-    "fw_debug_trace", "fw_debug_copy",
+    "fw_debug_trace", "fw_debug_copy", "fw_debug_timing", "fw_debug_timing_read",
 )
 
 
@@ -92,6 +92,9 @@ def load(path: Path | None = None) -> C.CDLL:
         "fw_destroy": (C.c_int, [H]),
         "fw_debug_trace": (C.c_int, [H, P]),
         "fw_debug_copy": (C.c_int, [H, C.c_int32, P, C.c_int64, P]),
+        "fw_debug_timing": (C.c_int, [H, C.c_int32]),
+        "fw_debug_timing_read": (C.c_int, [H, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                           C.POINTER(C.c_int64)]),
         "fw_last_error": (C.c_char_p, []),
         "fw_version": (C.c_int32, []),
     }

@@ -119,10 +119,21 @@ int validate_sampler(const fw_sampler* s) {
 int run_cell(Handle& h, const CellRun& run, cudaStream_t st) {
   cudaError_t e;
   int64_t launches = 0;
-  if (h.kernel == FW_KERNEL_TCGEN05)
+  if (h.kernel == FW_KERNEL_TCGEN05) {
     e = launch_cell_tc(h, run, st, &launches);
-  else
+    h.timed_steps = h.tev_used;
+  } else {
+    // one persistent launch covers every step: time it as a whole
+    const int timed = h.timing ? timing_reserve(h, 1) : 0;
+    if (timed) cudaEventRecord(h.tev[0], st);
     e = launch_cell_simt(h, run, st, &launches);
+    if (timed) {
+      cudaEventRecord(h.tev[1], st);
+      cudaEventRecord(h.tev[2], st);
+    }
+    h.tev_used = timed;
+    h.timed_steps = timed ? run.n_steps : 0;
+  }
   if (e != cudaSuccess) return cuda_fail(e, "cell kernel launch");
   h.last_launches = launches;
   h.t += run.n_steps;
@@ -481,6 +492,33 @@ int fw_debug_trace(fw_handle* fh, int64_t* d_trace) {
   if (rc) return rc;
   if (fh->h.kernel != FW_KERNEL_TCGEN05) return invalid("phase trace needs the tcgen05 path");
   tc_set_trace(fh->h, reinterpret_cast<long long*>(d_trace));
+  return FW_OK;
+}
+
+int fw_debug_timing(fw_handle* fh, int32_t enable) {
+  int rc = check_handle(fh, false);
+  if (rc) return rc;
+  fh->h.timing = enable ? 1 : 0;
+  return FW_OK;
+}
+
+int fw_debug_timing_read(fw_handle* fh, double* chain_ms, double* step_ms, int64_t* steps) {
+  int rc = check_handle(fh, false);
+  if (rc) return rc;
+  if (!chain_ms || !step_ms || !steps) return invalid("null argument");
+  Handle& h = fh->h;
+  *chain_ms = *step_ms = 0.0;
+  *steps = h.timed_steps;
+  if (h.tev_used == 0) return FW_OK;
+  FW_CUDA(cudaSetDevice(h.device));
+  FW_CUDA(cudaEventSynchronize(h.tev[3 * h.tev_used - 1]));
+  for (int i = 0; i < h.tev_used; ++i) {
+    float a = 0.f, b = 0.f;
+    FW_CUDA(cudaEventElapsedTime(&a, h.tev[3 * i], h.tev[3 * i + 1]));
+    FW_CUDA(cudaEventElapsedTime(&b, h.tev[3 * i], h.tev[3 * i + 2]));
+    *chain_ms += a;
+    *step_ms += b;
+  }
   return FW_OK;
 }
 

@@ -586,9 +586,12 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   h2.stream_offset = run.stream_offset;
   h2.cls_next = tc->cls;
   const dim3 gskip(tc->ntile, S / 128), gh1(tc->ntile, H / 128), gh2(tc->ntile, 1);
+  const int timed = h.timing ? timing_reserve(h, run.n_steps) : 0;
   for (int i = 0; i < run.n_steps; ++i) {
     for (int l = 0; l < L; ++l) ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)B * kR;
+    if (i < timed) cudaEventRecord(h.tev[3 * i], st);
     chain_kernel<<<tc->ntile, kChainThreads, kChainSmem, st>>>(ca);
+    if (i < timed) cudaEventRecord(h.tev[3 * i + 1], st);
     gemm_kernel<128, 0><<<gskip, kGemmThreads, gemm_smem<128>(), st>>>(skip);
     gemm_kernel<128, 0><<<gh1, kGemmThreads, gemm_smem<128>(), st>>>(h1);
     h2.t = run.t0 + i;
@@ -596,7 +599,9 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
     h2.out_cls = run.out + (size_t)i * B;
     h2.next_inputs = (i + 1 < run.n_inputs) ? run.inputs + (size_t)(i + 1) * B : nullptr;
     gemm_kernel<256, 1><<<gh2, kGemmThreads, gemm_smem<256>(), st>>>(h2);
+    if (i < timed) cudaEventRecord(h.tev[3 * i + 2], st);
   }
+  h.tev_used = timed;
   *launches = 4 * (int64_t)run.n_steps;
   return cudaGetLastError();
 }

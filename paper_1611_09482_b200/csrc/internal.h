@@ -140,7 +140,26 @@ struct Handle {
   // scratch for the *_host entry points
   int32_t* d_io = nullptr;
   int64_t d_io_elems = 0;
+
+  // optional per-step kernel timing (fw_debug_timing): events [3i] before the chain
+  // kernel of step i, [3i+1] after it, [3i+2] after the step's last kernel
+  int timing = 0;
+  std::vector<cudaEvent_t> tev;
+  int tev_used = 0;      // event triples recorded by the last call
+  int64_t timed_steps = 0;  // generation steps those triples cover
 };
+
+// Ensures events for up to min(steps, 1024) timed steps; returns how many steps are timed.
+inline int timing_reserve(Handle& h, int steps) {
+  const int n = steps < 1024 ? steps : 1024;
+  while ((int)h.tev.size() < 3 * n) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) break;
+    h.tev.push_back(e);
+  }
+  const int have = (int)h.tev.size() / 3;
+  return have < n ? have : n;
+}
 
 }  // namespace fw
 

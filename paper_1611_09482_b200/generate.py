@@ -97,6 +97,16 @@ class CellGenerator:
         _lib.check(self._lib.fw_last_launch_count(self._h, C.byref(v)))
         return v.value
 
+    def set_kernel_timing(self, enable: bool) -> None:
+        """Record CUDA events around each step's dominant kernel on later generate calls."""
+        _lib.check(self._lib.fw_debug_timing(self._h, 1 if enable else 0))
+
+    def kernel_times(self) -> tuple[float, float, int]:
+        """(dominant-kernel ms, whole-step ms, steps) of the last timed generate call."""
+        a, b, n = C.c_double(), C.c_double(), C.c_int64()
+        _lib.check(self._lib.fw_debug_timing_read(self._h, C.byref(a), C.byref(b), C.byref(n)))
+        return a.value, b.value, n.value
+
     def reset(self, stream=None) -> None:
         _lib.check(self._lib.fw_reset(self._h, _lib.stream_ptr(stream)))
 
