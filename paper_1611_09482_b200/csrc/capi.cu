@@ -191,8 +191,10 @@ int fw_cell_create(const fw_cell_desc* desc, int32_t batch, int32_t device, int3
     return code;
   };
   const bool bf = desc->weight_dtype == FW_DTYPE_BF16;
-  // queues: layer l holds d_l slots, each [ceil(B/128)][R/4][128][4] fp32 (R padded to a
-  // multiple of 4, streams to a multiple of 128): a 128-stream tile's slot is contiguous
+  // queues: layer l holds d_l slots. SIMT: each slot [ceil(B/128)][R/4][128][4] fp32 (R
+  // padded to a multiple of 4, streams to a multiple of 128). tcgen05: each slot
+  // [B/128][16][128][8] fp16 -- per tile 16 K-pieces of 8 channels for 128 rows (chain_tc.cuh).
+  // Either way a 128-stream tile's slot is contiguous.
   const int Rp = (R + 3) & ~3;
   const int64_t Bp = ((int64_t)batch + 127) / 128 * 128;
   std::vector<int64_t> qoff(L);
@@ -201,12 +203,12 @@ int fw_cell_create(const fw_cell_desc* desc, int32_t batch, int32_t device, int3
     qoff[l] = total;
     total += (int64_t)h.dil[l] * Bp * Rp;
   }
-  h.queue_elems = total;
+  h.queue_bytes = h.kernel == FW_KERNEL_TCGEN05 ? total * 2 : total * 4;
   if ((rc = upload(&h.d_dil, h.dil.data(), L))) return fail(rc);
   if ((rc = upload(&h.d_qoff, qoff.data(), L))) return fail(rc);
-  cudaError_t e = cudaMalloc(&h.d_queue, sizeof(float) * (size_t)total);
+  cudaError_t e = cudaMalloc(&h.d_queue, (size_t)h.queue_bytes);
   if (e != cudaSuccess) return fail(cuda_fail(e, "queue allocation"));
-  e = cudaMemset(h.d_queue, 0, sizeof(float) * (size_t)total);
+  e = cudaMemset(h.d_queue, 0, (size_t)h.queue_bytes);
   if (e != cudaSuccess) return fail(cuda_fail(e, "queue zero-fill"));
 
   // SIMT weights (also used by the tcgen05 path for nothing but kept small)
@@ -395,7 +397,7 @@ int fw_plain_create(const fw_plain_desc* d, int32_t batch, int32_t device, fw_ha
   if (e != cudaSuccess) return fail(cuda_fail(e, "queue allocation"));
   e = cudaMemset(p.queue, 0, sizeof(double) * (size_t)qt);
   if (e != cudaSuccess) return fail(cuda_fail(e, "queue zero-fill"));
-  h.queue_elems = qt;
+  h.queue_bytes = qt * 8;
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(cuda_fail(e, "create synchronize"));
   *out = fh;
@@ -479,9 +481,9 @@ int fw_reset(fw_handle* fh, void* stream) {
   FW_CUDA(cudaSetDevice(h.device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (h.is_plain)
-    FW_CUDA(cudaMemsetAsync(h.p.queue, 0, sizeof(double) * (size_t)h.queue_elems, st));
+    FW_CUDA(cudaMemsetAsync(h.p.queue, 0, (size_t)h.queue_bytes, st));
   else
-    FW_CUDA(cudaMemsetAsync(h.d_queue, 0, sizeof(float) * (size_t)h.queue_elems, st));
+    FW_CUDA(cudaMemsetAsync(h.d_queue, 0, (size_t)h.queue_bytes, st));
   h.t = 0;
   h.popped = 0;
   return FW_OK;
@@ -529,7 +531,7 @@ int fw_debug_copy(const fw_handle* fh, int32_t which, void* d_dst, int64_t bytes
   int64_t have = 0;
   if (which == 0) {
     src = h.is_plain ? (const void*)h.p.queue : (const void*)h.d_queue;
-    have = h.queue_elems * (h.is_plain ? 8 : 4);
+    have = h.queue_bytes;
   } else if (!h.is_plain && h.kernel == FW_KERNEL_TCGEN05) {
     have = tc_debug_buffer(const_cast<Handle&>(h), which, &src);
   }
@@ -549,7 +551,7 @@ int fw_step_index(const fw_handle* fh, int64_t* out) {
 
 int fw_queue_bytes(const fw_handle* fh, int64_t* out) {
   if (!fh || !out) return invalid("null argument");
-  *out = fh->h.queue_elems * (fh->h.is_plain ? 8 : 4);
+  *out = fh->h.queue_bytes;
   return FW_OK;
 }
 

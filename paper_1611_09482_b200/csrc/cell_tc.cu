@@ -1,16 +1,14 @@
-// K2: bf16 tcgen05 step kernels for large batches (BASELINE config 4).
+// K2: tcgen05 step kernels for large batches (BASELINE config 4).
 //
 // One generation step of B streams = four launches on the caller's stream:
 //
-//  1. chain  (B/128 CTAs, 320 threads): per 128-stream tile, the 40-layer
-//     dependent chain. Per layer: pop/push of the HBM ring slot (fp32, 16-byte
-//     accesses), x_t | x_{t-d} -> bf16 swizzled operand in smem, one
-//     tcgen05 MMA group [128 x 256] += [128 x 256] . [256 x 256]^T into TMEM,
-//     the tanh*sigmoid gate in the TMEM->register epilogue, z -> smem operand
-//     (+ a z stash in HBM), then the residual MMA [128 x 128] += z . W_res^T
-//     accumulating straight onto x, which lives in TMEM for the whole step.
-//     Weights stream through a 4-stage ring of 32 KB bulk copies (UBLKCP)
-//     issued by a producer warp; one elected thread issues the MMAs.
+//  1. chain  (B/128 CTAs, chain_tc.cuh): per 128-stream tile, the dependent chain of all
+//     L layers. Per layer: pop of the tile's ring slot (the fp16 x_{t-d} operand, loaded a
+//     layer ahead into registers and stored into TMEM), the dilated GEMM
+//     [128 x 256] += [128 x 256] . [256 x 256]^T in two N-halves into TMEM, the
+//     tanh*sigmoid gate in the TMEM->register epilogue, z -> smem operand (+ a z stash in
+//     HBM for the skip GEMM), the residual MMA [128 x 128] += z . W_res^T accumulating
+//     straight onto x, which lives in TMEM for the whole step, and the push of x_t.
 //  2. skip   GEMM  s = [z_0 .. z_{L-1}] . W_skip_cat^T + sum_l b_skip_l, ReLU
 //     (K = L*D = 5120): the skip sum of every layer done as ONE big-K GEMM on
 //     (B/128) x (S/128) CTAs instead of S more TMEM columns per layer.
@@ -19,8 +17,9 @@
 //     CDF / Gumbel-max with the counter hash) and teacher/feedback of the next
 //     input class.
 //
-// Numerics: bf16 operands, fp32 accumulation, fp32 residual stream (TMEM) and
-// fp32 queues, as BASELINE config 4 specifies; tanh via tanh.approx.f32.
+// Numerics: the bf16 weights exactly as fp16 MMA operands, activations rounded to fp16
+// operands, fp32 accumulation, fp32 residual stream (TMEM); queue slots hold the fp16
+// operand image of x (the precision the MMA consumes). DESIGN.md, "Numerics".
 #include <cuda_bf16.h>
 
 #include <cstring>
@@ -88,17 +87,18 @@ constexpr int kMaxChainLayers = 128;
 
 // Device-side phase trace (CTA 0 only, clock64 cycles), enabled by fw_debug_trace.
 // Per layer kTraceSlots entries; see tools/trace_chain.py for the slot meanings.
-constexpr int kTraceSlots = 24;
+constexpr int kTraceSlots = 32;
 enum TraceSlot {
   T_MMA_XD = 0, T_MMA_XT, T_MMA_ACC0, T_MMA_ACC1, T_MMA_Z0, T_MMA_Z1, T_MMA_XFULL, T_MMA_WWAIT,
-  T_EPI_A, T_EPI_XFULL, T_EPI_XT, T_EPI_GLOBAL, T_EPI_ACC0, T_EPI_Z0, T_EPI_ACC1, T_EPI_Z1,
-  T_Q_XD, T_Q_PUSHED, T_POP0, T_POP1, T_PROD_A, T_PROD_B, T_PROD_C, T_SPARE
+  T_EPI_A, T_EPI_XFULL, T_EPI_XT, T_EPI_ACC0, T_EPI_Z0, T_EPI_ACC1, T_EPI_Z1, T_H0_EARLY,
+  T_Q_XD, T_Q_LOAD, T_PROD_A0, T_PROD_A1, T_PROD_B, T_PROD_C, T_G0_LD, T_G0_MATH,
+  T_G0_STS, T_PUSHED, T_G1_LD, T_G1_MATH, T_G1_STS, T_SP1, T_SP2, T_SP3
 };
 
 struct ChainArgs {
   int B, L;
-  int64_t qbase[kMaxChainLayers];  // element offset of slot (t mod d_l) of layer l's ring
-  float* queue;
+  int64_t qbase[kMaxChainLayers];  // byte offset of slot (t mod d_l) of layer l's ring (tile 0)
+  uint8_t* queue;
   const uint8_t* w;
   const float* embed;  // [A][128]
   const float* dil_b;  // [L][256]
@@ -154,9 +154,10 @@ __device__ __forceinline__ void row_to_image(uint32_t img_saddr, int r, const fl
 
 // ---- generic [128 x BN] tile GEMM over pre-swizzled A/B images ----------------------
 struct GemmArgs {
-  const uint8_t* a;  // [mtiles][kch][16 KB]
+  const uint8_t* a;  // [mtiles][kch][16 KB]: SW128 images, or a_plain: [8 K-pieces][128][16 B]
   const uint8_t* b;  // [ntiles][kch][BN * 128 B]
   int kch;
+  int a_plain;
   const float* bias;  // [N]
   uint8_t* out_img;   // epi 0: [mtiles][N/64][16 KB]
   int n_total;
@@ -252,7 +253,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
         for (int c = 0; c < kGemmGroup; ++c)
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            mma_bf16(tmem, sdesc_sw128(sa + c * kTile + kk * 32),
+            mma_bf16(tmem,
+                     g.a_plain ? sdesc_plain(sa + c * kTile + kk * 4096, 2048, 128)
+                               : sdesc_sw128(sa + c * kTile + kk * 32),
                      sdesc_sw128(sb + c * (BN * 128) + kk * 32), id, (gi | c | kk) != 0);
         mma_commit(&empty[stage]);
       }
@@ -545,7 +548,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ChainArgs ca{};
   ca.B = B;
   ca.L = L;
-  ca.queue = h.d_queue;
+  ca.queue = reinterpret_cast<uint8_t*>(h.d_queue);
   ca.w = tc->wchain;
   ca.embed = h.w.embed;
   ca.dil_b = h.w.dil_b;
@@ -557,13 +560,14 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.trace = tc->trace;
   std::vector<int64_t> qoff(L);
   for (int l = 0, acc = 0; l < L; ++l) {
-    qoff[l] = (int64_t)acc * B * kR;
+    qoff[l] = (int64_t)acc * tc->ntile * kSlotBytes;
     acc += h.dil[l];
   }
   GemmArgs skip{};
   skip.a = tc->zimg;
   skip.b = tc->wskip;
   skip.kch = L * kD / 64;
+  skip.a_plain = 1;  // the chain kernel's z stash: [tile][L][16 K-pieces][128 rows][16 B]
   skip.bias = tc->skip_bsum;
   skip.out_img = tc->simg;
   skip.n_total = S;
@@ -588,7 +592,8 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   const dim3 gskip(tc->ntile, S / 128), gh1(tc->ntile, H / 128), gh2(tc->ntile, 1);
   const int timed = h.timing ? timing_reserve(h, run.n_steps) : 0;
   for (int i = 0; i < run.n_steps; ++i) {
-    for (int l = 0; l < L; ++l) ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)B * kR;
+    for (int l = 0; l < L; ++l)
+      ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)tc->ntile * kSlotBytes;
     if (i < timed) cudaEventRecord(h.tev[3 * i], st);
     chain_kernel<<<tc->ntile, kChainThreads, kChainSmem, st>>>(ca);
     if (i < timed) cudaEventRecord(h.tev[3 * i + 1], st);

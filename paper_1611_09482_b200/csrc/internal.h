@@ -129,7 +129,7 @@ struct Handle {
   int* d_dil = nullptr;
   int64_t* d_qoff = nullptr;
   float* d_queue = nullptr;
-  int64_t queue_elems = 0;
+  int64_t queue_bytes = 0;
   SimtWeights w{};
   TcState* tc = nullptr;
 

@@ -2,11 +2,12 @@
 
     python tools/trace_chain.py [--config cfg4] [--steps 3]
 
-Slots (csrc/cell_tc.cu TraceSlot): MMA thread -- xd_ready seen, xt_ready seen,
-acc0 committed, acc1 committed, z0 seen, z1 seen, x_full committed, cycles
-spent waiting on weight chunks; epilogue thread (warp 2 lane 0) -- xd arrive,
-x_full seen, xt arrive, global traffic issued, acc0 seen, z0 arrive, acc1
-seen, z1 arrive.
+Slots (csrc/cell_tc.cu TraceSlot): MMA warp -- x_{t-d} half 0 issued, xt_ready
+seen, acc0 committed, acc1 committed, z0 seen, z1 seen, x_full committed, cycles
+spent waiting on weights, whether half 0 was issued during the previous layer;
+gate thread (warp 2 lane 0) -- layer start, x_full seen, xt arrive, acc0 seen,
+z0 arrive, acc1 seen, z1 arrive; queue thread -- xd arrive, next slot loads
+issued; producer stage A0/A1/B/C issued.
 """
 
 import argparse
@@ -19,9 +20,11 @@ import torch
 sys.path.insert(0, ".")
 from paper_1611_09482_b200 import CellGenerator, Sampler, _lib, build_cell_model, configs  # noqa: E402
 
-NAMES = ["mma_xd", "mma_xt", "mma_acc0", "mma_acc1", "mma_z0", "mma_z1", "mma_xfull", "mma_wwait",
-         "epi_a", "epi_xfull", "epi_xt", "epi_glob", "epi_acc0", "epi_z0", "epi_acc1", "epi_z1",
-         "q_xd", "q_pushed", "pop0", "pop1", "prod_a", "prod_b", "prod_c", "spare"]
+NAMES = ["mma_xd", "mma_xt", "mma_acc0", "mma_acc1", "mma_z0", "mma_z1", "mma_xful", "mma_wwai",
+         "epi_a", "epi_xful", "epi_xt", "epi_acc0", "epi_z0", "epi_acc1", "epi_z1", "h0_early",
+         "q_xd", "q_load", "prod_a0", "prod_a1", "prod_b", "prod_c", "g0_ld", "g0_math",
+         "g0_sts", "pushed", "g1_ld", "g1_math", "g1_sts", "q_stash", "sp2", "sp3"]
+RAW = {7, 15}  # counts / flags, not timestamps
 SLOTS = len(NAMES)
 
 
@@ -48,7 +51,7 @@ def main():
         ref = row[8]
         cells = []
         for i, v in enumerate(row):
-            if i == 7:
+            if i in RAW:
                 cells.append(f"{v:8d}")
             elif v == 0:
                 cells.append(f"{'-':>8s}")
