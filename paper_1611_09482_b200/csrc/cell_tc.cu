@@ -560,7 +560,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.trace = tc->trace;
   std::vector<int64_t> qoff(L);
   for (int l = 0, acc = 0; l < L; ++l) {
-    qoff[l] = (int64_t)acc * tc->ntile * kSlotBytes;
+    qoff[l] = (int64_t)acc * (B / kChainRows) * kSlotBytes;
     acc += h.dil[l];
   }
   GemmArgs skip{};
@@ -593,9 +593,9 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   const int timed = h.timing ? timing_reserve(h, run.n_steps) : 0;
   for (int i = 0; i < run.n_steps; ++i) {
     for (int l = 0; l < L; ++l)
-      ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)tc->ntile * kSlotBytes;
+      ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)(B / kChainRows) * kSlotBytes;
     if (i < timed) cudaEventRecord(h.tev[3 * i], st);
-    chain_kernel<<<tc->ntile, kChainThreads, kChainSmem, st>>>(ca);
+    chain_kernel<<<B / kChainRows, kChainThreads, kChainSmem, st>>>(ca);
     if (i < timed) cudaEventRecord(h.tev[3 * i + 1], st);
     gemm_kernel<128, 0><<<gskip, kGemmThreads, gemm_smem<128>(), st>>>(skip);
     gemm_kernel<128, 0><<<gh1, kGemmThreads, gemm_smem<128>(), st>>>(h1);

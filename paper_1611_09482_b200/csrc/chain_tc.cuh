@@ -1,51 +1,71 @@
-// Chain kernel of the tcgen05 path (included by cell_tc.cu): one 128-stream tile per
-// CTA, the dependent chain of all L dilated layers of one generation step.
+// Chain kernel of the tcgen05 path (included by cell_tc.cu): one 64-stream tile per CTA,
+// the dependent chain of all L dilated layers of one generation step.
 //
 // Per layer l (a = W0 x_l[t] + W1 x_l[t-d] + b, z = tanh(a[:D]) * sigmoid(a[D:]),
-// x_{l+1} = x_l + W_res z + b_res; the skip/head work is deferred to big-K GEMMs):
+// x_{l+1} = x_l + W_res z + b_res; the skip/head work is deferred to big-K GEMMs).
 //
-//   TMEM (512 columns x 128 lanes, lane = stream row):
-//     [0,128)    acc0  dil N-half 0: tanh rows 0..63 | sigmoid rows 0..63
-//     [128,256)  acc1  dil N-half 1: tanh rows 64..127 | sigmoid rows 64..127
-//     [256,384)  x     residual stream x_l, fp32; the res MMA accumulates onto it
-//     [384,448)  xt/z  fp16 x_l[t] operand of the dilated MMAs, then (once those are done)
-//                      the fp16 z operand of the res MMA -- packed pairs
-//     [448,512)  xd    fp16 x_l[t-d] operand
-//   Every MMA takes its A operand from TMEM: an A operand in shared memory costs the
-//   tensor pipe ~107 instead of ~72 cycles per 128x128x16 MMA (tools/mma_latency.cu), and
-//   shared-memory bandwidth is what the weight stream needs. SMEM holds only the weight
-//   stages A0 / A1 (32 KB each: the x_{t-d} K-chunks of N-half 0 / 1), B (64 KB: the x_t
-//   K-chunks of both halves) and C (32 KB: res), one bulk copy each per layer (the copy
-//   engine costs ~500 cycles per operation almost regardless of size, tools/ring_bw.cu).
+// Why 64 streams per CTA: the chain is a serial dependency per layer (x -> MMA -> gate ->
+// res MMA -> x), and every MMA instruction costs ~72 cycles at N = 128 whether M is 64 or 128
+// (tools/mma_rate.cu). What scales with the rows is the gate (2 MUFU ops per z, 16 per clock
+// per SM: 1024 cycles per layer for 128 rows) and the activation traffic. 64-row tiles halve
+// those per SM and put twice as many SMs on the chain for the same MMA latency.
 //
-//   Queue slots hold x_l in fp16 (the precision the MMA consumes), 32 KB per tile laid out
-//   [16 K-pieces][128 rows][8 fp16] so that a warp's 16-byte accesses to one K-piece of 32
-//   consecutive rows are 512 contiguous bytes. The z stash for the skip GEMM uses the same
-//   layout per (tile, layer) -- the no-swizzle K-major UMMA layout (sdesc_plain).
+//   TMEM, M = 64: row m of the tile lives in lane (m % 16) + 32 * (m / 16) of plane P0 and the
+//   lane 16 above it in plane P1 (tools/m64_probe.cu). An MMA's TMEM A operand must sit in the
+//   plane of its accumulator, so the dilated GEMM lives in P0 and the residual GEMM in P1:
+//     P0 [0,128)    acc0  dil N-half 0: tanh rows 0..63 | sigmoid rows 0..63
+//     P0 [128,256)  acc1  dil N-half 1: tanh rows 64..127 | sigmoid rows 64..127
+//     P0 [256,320)  xt    fp16 x_l[t] operand (A from TMEM, packed pairs)
+//     P0 [320,384)  xd    fp16 x_l[t-d] operand
+//     P1 [0,128)    x     residual stream x_l, fp32; the res MMA accumulates onto it
+//     P1 [128,192)  z     fp16 z operand of the res MMA
+//   Gate and conversion use 16-lane (16x64b) accesses that touch one plane; the queue warps'
+//   32x32b accesses touch both, and the columns of the other plane under their regions are
+//   scratch. Every MMA takes A from TMEM (an SMEM A operand costs ~107 instead of ~72 cycles
+//   per MMA, tools/mma_latency.cu). SMEM holds only the weight stages A0 / A1 (32 KB each:
+//   the x_{t-d} K-chunks of N-half 0 / 1), B (64 KB: the x_t K-chunks of both halves) and C
+//   (32 KB: res), one bulk copy each per layer (~500 cycles per copy, tools/ring_bw.cu).
+//
+//   Queue slots hold x_l in fp16 (the precision the MMA consumes), 16 KB per tile laid out
+//   [16 K-pieces][64 rows][8 fp16]: a warp's 16-byte accesses to one K-piece of 16
+//   consecutive rows are 256 contiguous bytes. The z stash for the skip GEMM is laid out
+//   [tile pair][L][16 K-pieces][128 rows][16 B] -- per 128-row GEMM tile the no-swizzle
+//   K-major UMMA layout (sdesc_plain); tile 2p fills rows 0..63, tile 2p+1 rows 64..127.
 //
 //   warp 0  lane 0  weight producer (stages A0, A1, B, C in consumption order)
 //   warp 1          MMA issuer: the converged warp issues under elect.sync (tools/mma_rate.cu)
-//   warps 2..9      gate warps (row r = 32*(warp%4)+lane, column half h = (warp-2)/4):
-//                   x_l -> xt, then per N-half the gate of 32 z columns of row r
-//   warps 10..13    queue warps (one stream row each), all HBM traffic of the activations:
-//                   push x_l (TMEM xt -> ring slot), x_{t-d} of layer l+1 (registers, loaded
-//                   a layer ahead) -> TMEM xd once layer l's x_{t-d} MMAs are done, z stash
-//                   (TMEM z -> HBM); L2 prefetch of the slot two layers ahead
+//   warps 2..9      gate warps, quadrant q = warp % 4 (rows 16q..16q+15), half h = (warp-2)/4,
+//                   all accesses 16x64b -- every lane busy: lane t holds row (t>>2) + 8(t&1),
+//                   columns of parity (t>>1)&1; fp16 pairs are completed with one shuffle.
+//                   x_l (P1) -> xt (P0) for channels 64h..64h+63, then per N-half the gate of
+//                   16 z columns per lane (P0 acc -> P1 z)
+//   warps 10..13    queue warps (lanes 0..15 = rows of quadrant q): push x_l (xt -> ring
+//                   slot), x_{t-d} of layer l+1 (registers, loaded a layer ahead) -> xd once
+//                   layer l's x_{t-d} MMAs are done, z stash (z -> HBM); L2 prefetch of the
+//                   slot two layers ahead
 //
-// MMA issue order per layer: [xd_ready] x_{t-d} N-half 0 (normally issued during the
-// previous layer) -> [xt_ready] x_t N-half 0 -> acc0_full -> x_{t-d} N-half 1 -> x_t
-// N-half 1 -> acc1_full -> [z0_ready] res K-chunk 0, next layer's x_{t-d} N-half 0 if its
-// operands are in -> [z1_ready] res K-chunk 1 -> [z_read] x_full.
+// MMA issue order per layer: x_{t-d} halves 0 and 1 (normally issued during the previous
+// layer) -> [xt_ready] x_t N-half 0 -> acc0_full -> x_t N-half 1 -> acc1_full -> [z0_ready]
+// res K-chunk 0, next layer's x_{t-d} N-half 0 -> [z1_ready] res K-chunk 1 -> [x_pushed]
+// x_full -> next layer's x_{t-d} N-half 1.
 
+constexpr int kChainRows = 64;
 constexpr int kChainThreads = 448;
 constexpr int kQueueWarp0 = 10;
-constexpr uint32_t kColX = 256, kColXt = 384, kColZ = 384, kColXd = 448;
-constexpr uint32_t kSlotBytes = 32768;  // one tile's ring slot: [16 K-pieces][128 rows][8 fp16]
+constexpr uint32_t kP1 = 16u << 16;  // lane offset of plane P1
+constexpr uint32_t kColXt = 256, kColXd = 320;  // P0
+constexpr uint32_t kColX = 0, kColZ = 128;      // P1
+constexpr uint32_t kSlotBytes = 16384;  // one tile's ring slot: [16 K-pieces][64 rows][8 fp16]
 constexpr uint32_t kStageA = 32768, kStageB = 65536, kStageC = 32768;
-constexpr uint32_t kOffA0 = 0, kOffA1 = kOffA0 + kStageA,
-                   kOffB = kOffA1 + kStageA, kOffC = kOffB + kStageB,
-                   kOffBars = kOffC + kStageC;
+constexpr uint32_t kOffA0 = 0, kOffA1 = kOffA0 + kStageA, kOffB = kOffA1 + kStageA,
+                   kOffC = kOffB + kStageB, kOffBars = kOffC + kStageC;
 constexpr size_t kChainSmem = 1024 + kOffBars + 256;
+
+// z stash row base of (tile, layer): [tile pair][L][16 pieces][128 rows][16 B]
+__device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int L, int l) {
+  return reinterpret_cast<uint4*>(zimg + ((size_t)(tile >> 1) * L + l) * 2 * kTile) +
+         (tile & 1) * kChainRows;
+}
 
 __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -68,7 +88,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
   uint64_t* x_full = bars + 10;
   uint64_t* xd_ready = bars + 11;  // 128: queue warps (TMEM xd holds layer l's x_{t-d})
   uint64_t* x_pushed = bars + 12;  // 128: queue warps read xt (layer l's push issued)
-  uint64_t* z_read = bars + 13;    // 128: queue warps read the z columns (stash issued)
+  uint64_t* z_read = bars + 13;    // 128: queue warps read z (stash issued)
   uint64_t* xt_ready = bars + 14;  // 256: gate warps
   uint64_t* z0_ready = bars + 15;  // 256
   uint64_t* z1_ready = bars + 16;  // 256
@@ -120,9 +140,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       }
     }
   } else if (warp == 1) {  // ---- MMA issuer (whole warp; MMAs under elect.sync) ----
-    const uint32_t id = idesc_f16(128, 128);
-    const uint32_t sa0 = smem_u32(stA0), sa1 = smem_u32(stA1),
-                   sb = smem_u32(stB), sc = smem_u32(stC);
+    const uint32_t id = idesc_f16(kChainRows, 128);
+    const uint32_t sa0 = smem_u32(stA0), sa1 = smem_u32(stA1), sb = smem_u32(stB),
+                   sc = smem_u32(stC);
     long long wwait = 0;
     auto wait_w = [&](uint64_t* bar, uint32_t par) {
       const long long w0 = clock64();
@@ -130,7 +150,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       wwait += clock64() - w0;
       tc_fence_after();
     };
-    // one 64-K chunk: A from TMEM columns a_col.., B image at b_saddr
+    // one 64-K chunk: A from TMEM columns a_col.. (K 16 per 8 packed columns), B image
     auto mma_tmem_a = [&](uint32_t d, uint32_t a_col, uint32_t b_saddr) {
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk)
@@ -147,26 +167,27 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
                       id, (c | kk) ? 1u : 0u);
       mma_commit(hh ? emptyA1 : emptyA0);
     };
-    // warp-uniform non-blocking probe of layer lx's x_{t-d} operand and stage A0
-    auto xd_h0_ready = [&](int lx) {
+    // warp-uniform non-blocking probe: layer lx's x_{t-d} operand and weight stage
+    auto ready = [&](int lx, uint64_t* stage) {
       const uint32_t pn = (uint32_t)lx & 1;
-      int ok = lane == 0 ? (mbar_test(xd_ready, pn) && mbar_test(fullA0, pn)) : 0;
+      int ok = lane == 0 ? (mbar_test(xd_ready, pn) && mbar_test(stage, pn)) : 0;
       return __shfl_sync(0xffffffffu, ok, 0) != 0;
     };
-    bool h0_early = false;
+    bool early[2] = {false, false};
     for (int l = 0; l < L; ++l) {
       const uint32_t par = (uint32_t)l & 1;
       const bool nx = l + 1 < L;
-      if (lane == 0) trace_at(a, l, T_H0_EARLY, h0_early ? 1 : 0);
-      if (!h0_early) {
+      if (lane == 0) trace_at(a, l, T_H0_EARLY, (early[0] ? 1 : 0) + (early[1] ? 2 : 0));
+      if (!early[0] || !early[1]) {
         mbar_wait(xd_ready, par);
         tc_fence_after();
+      }
+      if (!early[0]) {
         wait_w(fullA0, par);
         if (elect_one()) xd_half(0);
         __syncwarp();
       }
       if (lane == 0) trace_at(a, l, T_MMA_XD, clock64());
-      h0_early = false;
       // x_t half 0: stage B chunks 0, 1
       mbar_wait(xt_ready, par);
       if (lane == 0) trace_at(a, l, T_MMA_XT, clock64());
@@ -177,13 +198,18 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
         mma_tmem_a(tmem + 0, tmem + kColXt + 32, sb + 1 * kChunk);
       }
       __syncwarp();
+      // the gate warps rewrite z after acc0_full: layer l-1's stash has read it
+      if (l > 0) mbar_wait(z_read, par ^ 1);
       if (elect_one()) mma_commit(acc0_full);
       __syncwarp();
       if (lane == 0) trace_at(a, l, T_MMA_ACC0, clock64());
-      // x_{t-d} half 1 + x_t half 1
-      wait_w(fullA1, par);
+      if (!early[1]) {
+        wait_w(fullA1, par);
+        if (elect_one()) xd_half(1);
+        __syncwarp();
+      }
+      early[0] = early[1] = false;
       if (elect_one()) {
-        xd_half(1);
         mma_tmem_a(tmem + 128, tmem + kColXt + 0, sb + 2 * kChunk);
         mma_tmem_a(tmem + 128, tmem + kColXt + 32, sb + 3 * kChunk);
         mma_commit(acc1_full);
@@ -191,21 +217,21 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       }
       __syncwarp();
       if (lane == 0) trace_at(a, l, T_MMA_ACC1, clock64());
-      // z halves: res MMA (all but the top layer), A = z columns in TMEM
+      // z halves: res MMA (all but the top layer), A = z and D = x in plane P1
       mbar_wait(z0_ready, par);
       if (lane == 0) trace_at(a, l, T_MMA_Z0, clock64());
       tc_fence_after();
       if (nx) {
         wait_w(fullC, par);
-        if (elect_one()) mma_tmem_a(tmem + kColX, tmem + kColZ + 0, sc + 0 * kChunk);
+        if (elect_one()) mma_tmem_a(tmem + kP1 + kColX, tmem + kP1 + kColZ + 0, sc + 0 * kChunk);
         __syncwarp();
-        // acc0 is free (gate half 0 done): start layer l+1's x_{t-d} N-half 0 now if its
-        // operand and weights are already in place -- never wait for them here
-        if (xd_h0_ready(l + 1)) {
+        // acc0 is free (gate half 0 done): layer l+1's x_{t-d} N-half 0 if its operand and
+        // weights are in place -- never wait for them here
+        if (ready(l + 1, fullA0)) {
           tc_fence_after();
           if (elect_one()) xd_half(0);
           __syncwarp();
-          h0_early = true;
+          early[0] = true;
         }
       }
       mbar_wait(z1_ready, par);
@@ -213,49 +239,58 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       tc_fence_after();
       if (nx) {
         if (elect_one()) {
-          mma_tmem_a(tmem + kColX, tmem + kColZ + 32, sc + 1 * kChunk);
+          mma_tmem_a(tmem + kP1 + kColX, tmem + kP1 + kColZ + 32, sc + 1 * kChunk);
           mma_commit(emptyC);
         }
         __syncwarp();
-        // the gate warps rewrite the xt/z columns after x_full: the z stash has read them
-        mbar_wait(z_read, par);
+        // the gate warps rewrite xt after x_full: this layer's push has read it
+        mbar_wait(x_pushed, par);
         if (elect_one()) mma_commit(x_full);
         __syncwarp();
         if (lane == 0) trace_at(a, l, T_MMA_XFULL, clock64());
-        if (!h0_early && xd_h0_ready(l + 1)) {
+        // acc1 is free (gate half 1 done): layer l+1's x_{t-d} halves still pending
+        if (!early[0] && ready(l + 1, fullA0)) {
           tc_fence_after();
           if (elect_one()) xd_half(0);
           __syncwarp();
-          h0_early = true;
+          early[0] = true;
+        }
+        if (ready(l + 1, fullA1)) {
+          tc_fence_after();
+          if (elect_one()) xd_half(1);
+          __syncwarp();
+          early[1] = true;
         }
       }
       if (lane == 0) trace_at(a, l, T_MMA_WWAIT, wwait);
     }
-    // the last layer's stash loads of the z columns precede the TMEM dealloc (final barrier)
   } else if (warp >= kQueueWarp0 && warp < kQueueWarp0 + 4) {
-    // ---- queue warps: one stream row per thread ----
-    const int sub = warp & 3;
-    const int r = sub * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
+    // ---- queue warps: lanes 0..15 own rows 16q..16q+15 (32x32b accesses; lanes 16..31
+    // see plane P1) ----
+    const int q = warp & 3;
+    const int r = q * 16 + (lane & 15);
+    const bool act = lane < 16;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const bool pf = warp == kQueueWarp0 && lane == 0;
     const bool tq = pf;
     const uint8_t* qtile = a.queue + (size_t)tile * kSlotBytes;
     if (pf)
       for (int l = 0; l < 2 && l < L; ++l) bulk_prefetch_l2(qtile + a.qbase[l], kSlotBytes);
-    // K-piece j (K 8j..8j+7) of row r is the 16 bytes at (j * 128 + r) * 16: packed words
+    // K-piece j (K 8j..8j+7) of row r is the 16 bytes at (j * 64 + r) * 16: packed words
     // 4j .. 4j+3 of the operand row
     uint32_t xd[64];
     auto load_slot = [&](int l) {
       const uint4* src = reinterpret_cast<const uint4*>(qtile + a.qbase[l]) + r;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const uint4 v = src[j * 128];
+        const uint4 v = act ? src[j * kChainRows] : make_uint4(0, 0, 0, 0);
         xd[4 * j] = v.x;
         xd[4 * j + 1] = v.y;
         xd[4 * j + 2] = v.z;
         xd[4 * j + 3] = v.w;
       }
     };
+    // (lanes 16..31 store zeros into P1's scratch columns under xd)
     auto store_xd = [&]() {
       tmem_st32(trow + kColXd, *reinterpret_cast<float(*)[32]>(xd));
       tmem_st32(trow + kColXd + 32, *reinterpret_cast<float(*)[32]>(xd + 32));
@@ -263,18 +298,21 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       tc_fence_before();
       mbar_arrive(xd_ready);
     };
-    // 64 TMEM columns of packed fp16 pairs (row r) -> 16 K-pieces at dst (+ j * 2 KB)
-    auto tmem_to_pieces = [&](uint32_t col, uint4* dst) {
+    // 64 TMEM columns of packed fp16 pairs (32x32b: lanes 0..15 read P0, 16..31 read P1)
+    // -> 16 K-pieces at dst (+ j * stride rows) from the lanes with `mine`
+    auto tmem_to_pieces = [&](uint32_t col, uint4* dst, int stride, bool mine) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float v[16];
         tmem_ld16(trow + col + 16 * c, v);
         tmem_wait_ld();
+        if (mine) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          dst[(4 * c + j) * 128] =
-              make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
-                         __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+          for (int j = 0; j < 4; ++j)
+            dst[(4 * c + j) * stride] =
+                make_uint4(__float_as_uint(v[4 * j]), __float_as_uint(v[4 * j + 1]),
+                           __float_as_uint(v[4 * j + 2]), __float_as_uint(v[4 * j + 3]));
+        }
       }
     };
     load_slot(0);
@@ -283,11 +321,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
     for (int l = 0; l < L; ++l) {
       const uint32_t par = (uint32_t)l & 1;
       if (pf && l + 2 < L) bulk_prefetch_l2(qtile + a.qbase[l + 2], kSlotBytes);
-      // push x_l (the xt operand columns) into ring slot (t mod d_l); this thread's own
+      // push x_l (P0 xt columns, lanes 0..15) into ring slot (t mod d_l); this thread's own
       // loads of that slot completed before store_xd of this layer
       mbar_wait(xt_ready, par);
       tc_fence_after();
-      tmem_to_pieces(kColXt, reinterpret_cast<uint4*>(const_cast<uint8_t*>(qtile) + a.qbase[l]) + r);
+      tmem_to_pieces(kColXt, reinterpret_cast<uint4*>(const_cast<uint8_t*>(qtile) + a.qbase[l]) + r,
+                     kChainRows, act);
       tc_fence_before();
       mbar_arrive(x_pushed);
       if (tq) trace_at(a, l, T_Q_LOAD, clock64());
@@ -299,101 +338,103 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
         if (tq) trace_at(a, l + 1, T_Q_XD, clock64());
         if (l + 2 < L) load_slot(l + 2);  // in flight during layer l+1
       }
-      // z stash of layer l for the skip GEMM: [tile][L][16 K-pieces][128 rows][16 B]
+      // z stash of layer l (P1 z columns: lanes 16..31 of the quadrant hold the rows)
       mbar_wait(z1_ready, par);
       tc_fence_after();
-      tmem_to_pieces(kColZ, reinterpret_cast<uint4*>(a.zimg + ((size_t)tile * L + l) * 2 * kTile) + r);
+      tmem_to_pieces(kColZ, zstash_rows(a.zimg, tile, L, l) + r, 2 * kChainRows, !act);
       tc_fence_before();
       mbar_arrive(z_read);
       if (tq) trace_at(a, l, T_SP1, clock64());
     }
   } else if (warp >= 2 && warp < 10) {
-    // ---- gate warps: (row r, column half h) ----
-    const int sub = warp & 3, h = (warp - 2) >> 2;
-    const int r = sub * 32 + lane;
-    const int stream = tile * 128 + r;
-    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
-    const int c = a.cls[stream];
+    // ---- gate warps: quadrant q, half h; 16x64b accesses: lane t holds row
+    // 16q + (t>>2) + 8(t&1), columns of parity (t>>1)&1 ----
+    const int q = warp & 3, h = (warp - 2) >> 2;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const int pc = (lane >> 1) & 1;
+    const int row = q * 16 + (lane >> 2) + 8 * (lane & 1);
+    const int c = a.cls[tile * kChainRows + row];
     const bool tr = (warp == 2 && lane == 0);
+    // pack own fp16 pairs (v[2i], v[2i+1]) -- columns 4i+pc, 4i+2+pc -- and complete the
+    // operand pairs with the partner lane (t ^ 2): parity 0 keeps the low halves (packed
+    // column 2i), parity 1 the high halves (packed column 2i+1)
+    auto pair_up = [&](uint32_t w) {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, w, 2);
+      return pc == 0 ? __byte_perm(w, o, 0x5410) : __byte_perm(o, w, 0x7632);
+    };
     for (int l = 0; l < L; ++l) {
       const uint32_t par = (uint32_t)l & 1;
       if (tr) trace_at(a, l, T_EPI_A, clock64());
-      // x_l: the embedding at l = 0, else the TMEM residual stream (+ the pending bias)
-      float x[64];
+      // x_l channels 64h + 2j + pc (j < 32): the embedding at l = 0, else the P1 residual
+      // stream (+ the pending bias)
+      uint32_t xv[32];
       if (l == 0) {
-        ld64(x, a.embed + (size_t)c * kR + 64 * h);
-        tmem_st32(trow + kColX + 64 * h, *reinterpret_cast<float(*)[32]>(x));
-        tmem_st32(trow + kColX + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
+        const float* e = a.embed + (size_t)c * kR + 64 * h + pc;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) xv[j] = __float_as_uint(__ldg(e + 2 * j));
+        tmem_st_16x64b_x32(trow + kP1 + kColX + 64 * h, xv);
       } else {
         mbar_wait(x_full, par ^ 1);
         if (tr) trace_at(a, l, T_EPI_XFULL, clock64());
         tc_fence_after();
-        tmem_ld32(trow + kColX + 64 * h, *reinterpret_cast<float(*)[32]>(x));
-        tmem_ld32(trow + kColX + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
+        tmem_ld_16x64b_x32(trow + kP1 + kColX + 64 * h, xv);
         tmem_wait_ld();
         if (a.has_res_bias) {
-          const float4* rb = reinterpret_cast<const float4*>(a.res_b + (size_t)(l - 1) * kR + 64 * h);
+          const float* rb = a.res_b + (size_t)(l - 1) * kR + 64 * h + pc;
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float4 b = __ldg(rb + i);
-            x[4 * i] += b.x;
-            x[4 * i + 1] += b.y;
-            x[4 * i + 2] += b.z;
-            x[4 * i + 3] += b.w;
-          }
-          tmem_st32(trow + kColX + 64 * h, *reinterpret_cast<float(*)[32]>(x));
-          tmem_st32(trow + kColX + 64 * h + 32, *reinterpret_cast<float(*)[32]>(x + 32));
+          for (int j = 0; j < 32; ++j)
+            xv[j] = __float_as_uint(__uint_as_float(xv[j]) + __ldg(rb + 2 * j));
+          tmem_st_16x64b_x32(trow + kP1 + kColX + 64 * h, xv);
         }
       }
       {
-        float xp[32];
+        uint32_t xp[16];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) xp[i] = __uint_as_float(pack_h2(x[2 * i], x[2 * i + 1]));
-        tmem_st32(trow + kColXt + 32 * h, xp);
+        for (int i = 0; i < 16; ++i)
+          xp[i] = pair_up(pack_h2(__uint_as_float(xv[2 * i]), __uint_as_float(xv[2 * i + 1])));
+        tmem_st_16x64b_x16(trow + kColXt + 32 * h, xp);
       }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(xt_ready);
       if (tr) trace_at(a, l, T_EPI_XT, clock64());
-      // gate of N-half hh -> z columns 64*hh + [32h, 32h+32) -> TMEM z columns
-      // kColZ + 32*hh + 16*h .. +16 (packed pairs; z shares the columns of xt)
+      // gate of N-half hh: this lane's 16 z columns 64hh + 32h + 2j + pc, j < 16
       const float* bd = a.dil_b + (size_t)l * 2 * kD;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
         mbar_wait(hh == 0 ? acc0_full : acc1_full, par);
         if (tr) trace_at(a, l, hh == 0 ? T_EPI_ACC0 : T_EPI_ACC1, clock64());
         tc_fence_after();
-        float at[32], as[32];
-        tmem_ld32(trow + 128 * hh + 32 * h, at);
-        tmem_ld32(trow + 128 * hh + 64 + 32 * h, as);
+        uint32_t ta[16], sa[16];
+        tmem_ld_16x64b_x16(trow + 128 * hh + 32 * h, ta);
+        tmem_ld_16x64b_x16(trow + 128 * hh + 64 + 32 * h, sa);
         tmem_wait_ld();
         if (tr) trace_at(a, l, hh == 0 ? T_G0_LD : T_G1_LD, clock64());
-        if (a.has_dil_bias) {
-          const int j0 = 64 * hh + 32 * h;
+        float at[16], as[16];
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            at[i] += __ldg(bd + j0 + i);
-            as[i] += __ldg(bd + kD + j0 + i);
+        for (int j = 0; j < 16; ++j) {
+          at[j] = __uint_as_float(ta[j]);
+          as[j] = __uint_as_float(sa[j]);
+        }
+        if (a.has_dil_bias) {
+          const int j0 = 64 * hh + 32 * h + pc;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            at[j] += __ldg(bd + j0 + 2 * j);
+            as[j] += __ldg(bd + kD + j0 + 2 * j);
           }
         }
-        float pk[16];
+        // z = tanh(a) * sigmoid(b) with sigmoid(b) = 0.5 + 0.5 tanh(b / 2), evaluated for
+        // an element pair in packed fp16 (z's operand precision)
+        uint32_t zw[8];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2)
-          // z = tanh(a) * sigmoid(b) with sigmoid(b) = 0.5 + 0.5 tanh(b / 2), evaluated for
-          // an element pair in packed fp16 (z's operand precision)
-          pk[i >> 1] = __uint_as_float(gate2_h2(at[i], at[i + 1], as[i], as[i + 1]));
+        for (int i = 0; i < 8; ++i)
+          zw[i] = pair_up(gate2_h2(at[2 * i], at[2 * i + 1], as[2 * i], as[2 * i + 1]));
         if (tr) {
-          asm volatile("" ::"f"(pk[0]), "f"(pk[15]) : "memory");
+          asm volatile("" ::"r"(zw[0]), "r"(zw[7]) : "memory");
           trace_at(a, l, hh == 0 ? T_G0_MATH : T_G1_MATH, clock64());
         }
-        if (hh == 0) {
-          // z half 0 overwrites the xt operand: the x_t MMAs of N-half 1 (acc1_full) and the
-          // queue push have read it
-          mbar_wait(acc1_full, par);
-          mbar_wait(x_pushed, par);
-          tc_fence_after();
-        }
-        tmem_st16(trow + kColZ + 32 * hh + 16 * h, pk);
+        tmem_st_16x64b_x8(trow + kP1 + kColZ + 32 * hh + 16 * h, zw);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(hh == 0 ? z0_ready : z1_ready);
