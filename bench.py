@@ -139,7 +139,7 @@ def dominant_accounting(cell, batch, kernel):
 
 def traffic_per_launch(kernel):
     """DRAM bytes of one dominant-kernel launch from the newest committed ncu summary."""
-    want = "chain_kernel" if kernel == "tcgen05" else "cell_simt_kernel"
+    want = "step_kernel" if kernel == "tcgen05" else "cell_simt_kernel"
     for f in sorted((ROOT / "profiles").glob("ncu_summary_*.json"), reverse=True):
         try:
             d = json.loads(f.read_text())
@@ -349,7 +349,7 @@ def main():
         roof["frac"] = roof["achieved"] / roof["peak"]
         traffic, tsrc = traffic_per_launch(kname)
         roof["traffic"] = traffic
-        roof["kernel"] = ("chain_kernel (one launch per step)" if kname == "tcgen05"
+        roof["kernel"] = ("step_kernel (chain + fused skip, one launch per step)" if kname == "tcgen05"
                           else "cell_simt_kernel (one launch per generate call, per-step share)")
         roof["algorithmic_per_step"] = {"flop": k_flops, "bytes": k_bytes}
         roof["kernel_us_per_step"] = 1e6 * k_s

@@ -33,7 +33,10 @@ namespace fw {
 struct TcState {
   int ntile = 0;
   uint8_t* wchain = nullptr;  // per layer: 10 chunks [128][64] in MMA issue order
-  uint8_t* wskip = nullptr;   // [S/128][L*D/64] chunks of [128][64]
+  uint8_t* wskip = nullptr;   // [S/128][L*D/64] chunks of [128][64] (unfused skip GEMM)
+  uint8_t* wskip2 = nullptr;  // [S/SK][L][2][SK][64] (fused skip role of the step kernel)
+  uint32_t* zflag = nullptr;  // [B/128] z stash counters of the fused skip role
+  int fused = 0, SK = 256, nchain = 0, nskip = 0;
   uint8_t* wh1 = nullptr;     // [H/128][S/64] chunks of [128][64]
   uint8_t* wh2 = nullptr;     // [H/64] chunks of [A=256][64]
   float* skip_bsum = nullptr;  // [S]
@@ -107,6 +110,13 @@ struct ChainArgs {
   uint8_t* zimg;
   int has_dil_bias, has_res_bias;
   long long* trace;  // [L][kTraceSlots] or null
+  // fused skip role (zflag != null): blocks >= nchain accumulate the skip sum
+  int nchain;
+  uint32_t* zflag;         // [B/128] per tile pair: chain tiles x layers stashed this step
+  const uint8_t* wskip2;   // [S/SK][L][2 K-chunks][SK rows][128 B]
+  const float* skip_bsum;  // [S]
+  uint8_t* simg;           // head1's A images [B/128][S/64][16 KB]
+  int S, SK;
 };
 
 __device__ __forceinline__ void trace_at(const ChainArgs& a, int l, int slot, long long v) {
@@ -240,15 +250,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
                  &full[stage]);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t id = idesc_f16(128, BN);
-      const uint32_t s0 = smem_u32(smem);
-      for (int gi = 0; gi < groups; ++gi) {
-        const int stage = gi % S;
-        mbar_wait(&full[stage], (uint32_t)(gi / S) & 1);
-        tc_fence_after();
-        const uint32_t sa = s0 + stage * SB, sb = sa + A_BYTES;
+  } else if (warp == 1) {  // MMA issuer: the converged warp, MMAs under elect.sync
+    const uint32_t id = idesc_f16(128, BN);
+    const uint32_t s0 = smem_u32(smem);
+    for (int gi = 0; gi < groups; ++gi) {
+      const int stage = gi % S;
+      mbar_wait(&full[stage], (uint32_t)(gi / S) & 1);
+      tc_fence_after();
+      const uint32_t sa = s0 + stage * SB, sb = sa + A_BYTES;
+      if (elect_one()) {
 #pragma unroll
         for (int c = 0; c < kGemmGroup; ++c)
 #pragma unroll
@@ -259,8 +269,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
                      sdesc_sw128(sb + c * (BN * 128) + kk * 32), id, (gi | c | kk) != 0);
         mma_commit(&empty[stage]);
       }
-      mma_commit(acc_full);
+      __syncwarp();
     }
+    if (elect_one()) mma_commit(acc_full);
     __syncwarp();
   } else {
     const int sub = warp & 3, h = (warp - 2) >> 2;
@@ -491,6 +502,26 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
         });
     if (int rc = upload_bytes(&tc->wskip, img)) return rc;
   }
+  // fused skip role: one block per (128-row tile pair, SK-column block of S) next to the
+  // B/64 chain blocks, all co-resident (cooperative launch) when the SMs suffice
+  {
+    tc->SK = (S % 256 == 0) ? 256 : 128;
+    tc->nchain = h.batch / kChainRows;
+    tc->nskip = (h.batch / 128) * (S / tc->SK);
+    int sms = 0, coop = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h.device);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, h.device);
+    tc->fused = coop && (tc->nchain + tc->nskip <= sms);
+    const int SK = tc->SK;
+    std::vector<uint8_t> img((size_t)(S / SK) * L * 2 * SK * 128);
+    for (int e = 0; e < S / SK; ++e)
+      for (int l = 0; l < L; ++l)
+        for (int c = 0; c < 2; ++c)
+          pack_image(img.data() + (((size_t)e * L + l) * 2 + c) * SK * 128, SK, c * 64,
+                     [&](int n, int k) { return desc->skip_w[((size_t)l * S + e * SK + n) * kD + k]; });
+    if (int rc = upload_bytes(&tc->wskip2, img)) return rc;
+    if (int rc = dev_alloc(&tc->zflag, sizeof(uint32_t) * (h.batch / 128))) return rc;
+  }
   {
     std::vector<uint8_t> img((size_t)(H / 128) * (S / 64) * kTile);
     for (int nb = 0; nb < H / 128; ++nb)
@@ -517,7 +548,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
   if (int rc = dev_alloc(&tc->simg, (size_t)tc->ntile * (S / 64) * kTile)) return rc;
   if (int rc = dev_alloc(&tc->himg, (size_t)tc->ntile * (H / 64) * kTile)) return rc;
   if (int rc = dev_alloc(&tc->cls, sizeof(int32_t) * h.batch)) return rc;
-  cudaError_t e = set_smem(chain_kernel, kChainSmem);
+  cudaError_t e = set_smem(step_kernel, kChainSmem);
   if (e == cudaSuccess) e = set_smem(gemm_kernel<128, 0>, gemm_smem<128>());
   if (e == cudaSuccess) e = set_smem(gemm_kernel<256, 1>, gemm_smem<256>());
   if (e != cudaSuccess) {
@@ -530,7 +561,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
 void tc_destroy(Handle& h) {
   TcState* tc = h.tc;
   if (!tc) return;
-  void* ptrs[] = {tc->wchain, tc->wskip, tc->wh1, tc->wh2, tc->skip_bsum,
+  void* ptrs[] = {tc->wchain, tc->wskip, tc->wskip2, tc->zflag, tc->wh1, tc->wh2, tc->skip_bsum,
                   tc->zimg, tc->simg, tc->himg, tc->cls};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -558,6 +589,15 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.has_dil_bias = tc->has_dil_bias;
   ca.has_res_bias = tc->has_res_bias;
   ca.trace = tc->trace;
+  ca.nchain = B / kChainRows;
+  ca.zflag = tc->fused ? tc->zflag : nullptr;
+  ca.wskip2 = tc->wskip2;
+  ca.skip_bsum = tc->skip_bsum;
+  ca.simg = tc->simg;
+  ca.S = S;
+  ca.SK = tc->SK;
+  const int grid = tc->fused ? tc->nchain + tc->nskip : tc->nchain;
+  void* kargs[] = {&ca};
   std::vector<int64_t> qoff(L);
   for (int l = 0, acc = 0; l < L; ++l) {
     qoff[l] = (int64_t)acc * (B / kChainRows) * kSlotBytes;
@@ -594,10 +634,20 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   for (int i = 0; i < run.n_steps; ++i) {
     for (int l = 0; l < L; ++l)
       ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)(B / kChainRows) * kSlotBytes;
+    if (tc->fused) {
+      cudaError_t me = cudaMemsetAsync(tc->zflag, 0, sizeof(uint32_t) * (B / 128), st);
+      if (me != cudaSuccess) return me;
+    }
     if (i < timed) cudaEventRecord(h.tev[3 * i], st);
-    chain_kernel<<<B / kChainRows, kChainThreads, kChainSmem, st>>>(ca);
+    if (tc->fused) {
+      cudaError_t le = cudaLaunchCooperativeKernel((const void*)step_kernel, dim3(grid),
+                                                   dim3(kChainThreads), kargs, kChainSmem, st);
+      if (le != cudaSuccess) return le;
+    } else {
+      step_kernel<<<grid, kChainThreads, kChainSmem, st>>>(ca);
+    }
     if (i < timed) cudaEventRecord(h.tev[3 * i + 1], st);
-    gemm_kernel<128, 0><<<gskip, kGemmThreads, gemm_smem<128>(), st>>>(skip);
+    if (!tc->fused) gemm_kernel<128, 0><<<gskip, kGemmThreads, gemm_smem<128>(), st>>>(skip);
     gemm_kernel<128, 0><<<gh1, kGemmThreads, gemm_smem<128>(), st>>>(h1);
     h2.t = run.t0 + i;
     h2.logits = (run.logits && i < run.n_logit_steps) ? run.logits + (size_t)i * B * d.A : nullptr;
@@ -607,7 +657,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
     if (i < timed) cudaEventRecord(h.tev[3 * i + 2], st);
   }
   h.tev_used = timed;
-  *launches = 4 * (int64_t)run.n_steps;
+  *launches = (tc->fused ? 3 : 4) * (int64_t)run.n_steps;
   return cudaGetLastError();
 }
 

@@ -59,7 +59,10 @@ constexpr uint32_t kSlotBytes = 16384;  // one tile's ring slot: [16 K-pieces][6
 constexpr uint32_t kStageA = 32768, kStageB = 65536, kStageC = 32768;
 constexpr uint32_t kOffA0 = 0, kOffA1 = kOffA0 + kStageA, kOffB = kOffA1 + kStageA,
                    kOffC = kOffB + kStageB, kOffBars = kOffC + kStageC;
-constexpr size_t kChainSmem = 1024 + kOffBars + 256;
+// skip role: a 2-stage ring of (z tile 32 KB | W_skip block SK x 128 x 2 B, <= 64 KB)
+constexpr uint32_t kSkipStage = 2 * kTile + 65536;
+constexpr uint32_t kSkipBars = 2 * kSkipStage;
+constexpr size_t kChainSmem = 1024 + (kOffBars > kSkipBars ? kOffBars : kSkipBars) + 256;
 
 // z stash row base of (tile, layer): [tile pair][L][16 pieces][128 rows][16 B]
 __device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int L, int l) {
@@ -67,9 +70,104 @@ __device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int L, in
          (tile & 1) * kChainRows;
 }
 
-__global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
+// ---- skip role: s = ReLU(sum_l W_skip_l z_l + sum_l b_skip_l) for one 128-row tile pair and
+// one SK-column block of S, accumulated in TMEM layer by layer as the chain CTAs stash z_l
+// (a per-pair counter in global memory, +1 per chain tile per layer). Runs on SMs the chain
+// leaves idle, so the skip GEMM costs no time after the chain ends.
+__device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int k) {
+  const int SK = a.SK, nsk = a.S / SK;
+  const int p = k / nsk, e = k % nsk;
+  const int L = a.L;
+  const uint32_t bbytes = (uint32_t)SK * 256;  // 2 K-chunks of [SK rows][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kSkipBars);
+  uint64_t* full = bars;       // [2]
+  uint64_t* empty = bars + 2;  // [2]
+  uint64_t* acc_full = bars + 4;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 5);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 5; ++i) mbar_init(bars + i, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 256);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  if (warp == 0) {
+    if (lane == 0) {  // producer: z tile of (p, l) once both chain tiles stashed it
+      for (int l = 0; l < L; ++l) {
+        const int st = l & 1;
+        mbar_wait(empty + st, ((uint32_t)(l >> 1) & 1) ^ 1);
+        wait_counter(a.zflag + p, 2u * (uint32_t)(l + 1));
+        fence_proxy_async_all();
+        uint8_t* stage = smem + st * kSkipStage;
+        mbar_arrive_expect_tx(full + st, 2 * kTile + bbytes);
+        bulk_g2s(stage, a.zimg + ((size_t)p * L + l) * 2 * kTile, 2 * kTile, full + st);
+        bulk_g2s(stage + 2 * kTile, a.wskip2 + ((size_t)e * L + l) * bbytes, bbytes, full + st);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t id = idesc_f16(128, SK);
+    const uint32_t s0 = smem_u32(smem);
+    for (int l = 0; l < L; ++l) {
+      const int st = l & 1;
+      mbar_wait(full + st, (uint32_t)(l >> 1) & 1);
+      tc_fence_after();
+      const uint32_t sa = s0 + st * kSkipStage, sb = sa + 2 * kTile;
+      if (elect_one()) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            mma_bf16(tmem, sdesc_plain(sa + c * kTile + kk * 4096, 2048, 128),
+                     sdesc_sw128(sb + c * (uint32_t)SK * 128 + kk * 32), id, (l | c | kk) != 0);
+        mma_commit(empty + st);
+      }
+      __syncwarp();
+    }
+    if (elect_one()) mma_commit(acc_full);
+    __syncwarp();
+  } else if (warp >= 2 && warp < 10) {
+    // epilogue: row r, columns [h*SK/2, (h+1)*SK/2) -> bias + ReLU -> head1's A image
+    const int sub = warp & 3, h = (warp - 2) >> 2;
+    const int r = sub * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
+    mbar_wait(acc_full, 0);
+    tc_fence_after();
+    const int half = SK / 2;
+    for (int cc = 0; cc < half / 64; ++cc) {
+      float v[64];
+      tmem_ld32(trow + h * half + 64 * cc, *reinterpret_cast<float(*)[32]>(v));
+      tmem_ld32(trow + h * half + 64 * cc + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+      tmem_wait_ld();
+      const int n0 = e * SK + h * half + 64 * cc;
+#pragma unroll
+      for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + __ldg(a.skip_bsum + n0 + i), 0.f);
+      uint8_t* dst = a.simg + ((size_t)p * (a.S / 64) + n0 / 64) * kTile;
+#pragma unroll
+      for (int pp = 0; pp < 8; ++pp)
+        *reinterpret_cast<uint4*>(dst + swz(r, pp)) =
+            make_uint4(pack_h2(v[8 * pp], v[8 * pp + 1]), pack_h2(v[8 * pp + 2], v[8 * pp + 3]),
+                       pack_h2(v[8 * pp + 4], v[8 * pp + 5]), pack_h2(v[8 * pp + 6], v[8 * pp + 7]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 1) tmem_dealloc(tmem, 256);
+}
+
+// One launch per step: blocks [0, nchain) run the chain of one 64-stream tile each, blocks
+// [nchain, nchain + nskip) the skip role (when fused; launched cooperatively so that all
+// blocks are co-resident -- the skip blocks wait on the chain blocks).
+__global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
+  if ((int)blockIdx.x >= a.nchain) {
+    skip_role(a, smem, (int)blockIdx.x - a.nchain);
+    return;
+  }
   uint8_t* stA0 = smem + kOffA0;
   uint8_t* stA1 = smem + kOffA1;
   uint8_t* stB = smem + kOffB;
@@ -344,6 +442,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) chain_kernel(ChainArgs a) {
       tmem_to_pieces(kColZ, zstash_rows(a.zimg, tile, L, l) + r, 2 * kChainRows, !act);
       tc_fence_before();
       mbar_arrive(z_read);
+      if (a.zflag != nullptr) {  // publish z_l of this tile to the skip blocks
+        named_bar_sync(1, 128);
+        if (warp == kQueueWarp0 && lane == 0) red_release_gpu(a.zflag + (tile >> 1), 1u);
+      }
       if (tq) trace_at(a, l, T_SP1, clock64());
     }
   } else if (warp >= 2 && warp < 10) {

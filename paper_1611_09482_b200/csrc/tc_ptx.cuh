@@ -97,6 +97,34 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- inter-CTA signalling (global-memory flags) -------------------------------------------
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+// Release increment of a global counter: fence.acq_rel.gpu + relaxed red (the pattern of
+// CUTLASS's GenericBarrier); after a CTA barrier it publishes the writes of all its threads.
+__device__ __forceinline__ void red_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Generic-proxy writes (seen through an acquire) -> later async-proxy (TMA) reads.
+__device__ __forceinline__ void fence_proxy_async_all() {
+  asm volatile("fence.proxy.async;" ::: "memory");
+}
+// Spin until *p >= target; traps after ~4 s (2^33 cycles) instead of hanging the GPU.
+__device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t target) {
+  const long long t0 = clock64();
+  while (ld_acquire_gpu(p) < target) {
+    __nanosleep(64);
+    if (clock64() - t0 > (1ll << 33)) __trap();
+  }
+}
+
 // One lane of a converged warp (the warp's leader). tcgen05.mma issued under elect.sync from
 // a converged warp runs back to back; issued from a lone divergent thread, ptxas wraps every
 // MMA in an ELECT loop and the tensor pipe sees ~95-115 cycles per M=128 MMA instead of
