@@ -37,6 +37,8 @@ struct TcState {
   uint8_t* wskip2 = nullptr;  // [S/SK][L][2][SK][64] (fused skip role of the step kernel)
   uint32_t* zflag = nullptr;  // [B/128] z stash counters of the fused skip role
   int fused = 0, SK = 256, nchain = 0, nskip = 0;
+  int heads = 0;              // head1 / head2 fused into the skip blocks (needs fused)
+  uint8_t* wh1b = nullptr;    // [nsk][S/64][H/nsk rows][128 B] (fused head1)
   uint8_t* wh1 = nullptr;     // [H/128][S/64] chunks of [128][64]
   uint8_t* wh2 = nullptr;     // [H/64] chunks of [A=256][64]
   float* skip_bsum = nullptr;  // [S]
@@ -98,6 +100,19 @@ enum TraceSlot {
   T_G0_STS, T_PUSHED, T_G1_LD, T_G1_MATH, T_G1_STS, T_SP1, T_SP2, T_SP3
 };
 
+// head2 + selection of one step (shared by the head2 GEMM kernel and the fused tail)
+struct SelectArgs {
+  const float* bias;           // [A]
+  float* logits;               // [B][A] for this step or null
+  int32_t* out_cls;            // [B] this step's selected classes
+  int32_t* cls_next;           // [B] next step's input classes
+  const int32_t* next_inputs;  // teacher row for the next step or null
+  int A, mode;
+  uint32_t seed;
+  int64_t stream_offset;
+  int64_t t;
+};
+
 struct ChainArgs {
   int B, L;
   int64_t qbase[kMaxChainLayers];  // byte offset of slot (t mod d_l) of layer l's ring (tile 0)
@@ -117,10 +132,26 @@ struct ChainArgs {
   const float* skip_bsum;  // [S]
   uint8_t* simg;           // head1's A images [B/128][S/64][16 KB]
   int S, SK;
+  // fused heads (heads != 0): head1 by the pair's skip blocks (H / nsk columns each), head2
+  // + selection by its first skip block; sflag / hflag count the blocks done with simg / himg
+  int heads, H;
+  uint32_t* sflag;       // [B/128]
+  uint32_t* hflag;       // [B/128]
+  const uint8_t* wh1b;   // [nsk][S/64][H/nsk rows][128 B]
+  const uint8_t* wh2;    // [H/64][A rows][128 B]
+  const float* h1_b;     // [H]
+  uint8_t* himg;         // head2's A images [B/128][H/64][16 KB]
+  SelectArgs sel;
 };
 
 __device__ __forceinline__ void trace_at(const ChainArgs& a, int l, int slot, long long v) {
   if (a.trace != nullptr && blockIdx.x == 0) a.trace[l * kTraceSlots + slot] = v;
+}
+// Step timeline in global time (ns): row L of the trace, written by chain block 0 and the
+// first skip block (tools/trace_chain.py). Slots: 0 chain start, 1 chain last layer done,
+// 2 skip: last z tile seen, 3 s published, 4 head1 done, 5 head2 accumulator, 6 selection done
+__device__ __forceinline__ void trace_g(const ChainArgs& a, bool who, int slot) {
+  if (a.trace != nullptr && who) a.trace[a.L * kTraceSlots + slot] = globaltimer_ns();
 }
 
 __device__ __forceinline__ void ld64(float (&v)[64], const float* p) {
@@ -160,6 +191,140 @@ __device__ __forceinline__ void row_to_image(uint32_t img_saddr, int r, const fl
                  pack_h2(v[8 * p + 6], v[8 * p + 7]));
 }
 
+// Gumbel noise -log(-log u) of class cls; v + gumbel_noise(...) == v - log(-log u) exactly.
+__device__ __forceinline__ float gumbel_noise(uint32_t prefix, int cls) {
+  const float u = noise_uniform(prefix, (uint32_t)cls);
+  return -__logf(-__logf(u));
+}
+
+// ReLU(acc + bias) of TMEM columns [c0, c0 + ncols) of row r -> fp16 SW128 image chunks;
+// column c0 + j is global column n0 + j, in chunk (n0 + j) / 64 of the tile's images at img.
+__device__ __forceinline__ void epi_relu_image(uint32_t trow, int r, int c0, int ncols, int n0,
+                                               const float* bias, uint8_t* img) {
+  for (int cc = 0; cc < ncols / 64; ++cc) {
+    float v[64];
+    tmem_ld32(trow + c0 + 64 * cc, *reinterpret_cast<float(*)[32]>(v));
+    tmem_ld32(trow + c0 + 64 * cc + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+    tmem_wait_ld();
+    const int n = n0 + 64 * cc;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + bias[n + i], 0.f);
+    uint8_t* dst = img + (size_t)(n / 64) * kTile;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+      *reinterpret_cast<uint4*>(dst + swz(r, p)) =
+          make_uint4(pack_h2(v[8 * p], v[8 * p + 1]), pack_h2(v[8 * p + 2], v[8 * p + 3]),
+                     pack_h2(v[8 * p + 4], v[8 * p + 5]), pack_h2(v[8 * p + 6], v[8 * p + 7]));
+  }
+}
+
+// Same, into a shared-memory copy of the images (chunk j of the thread's columns at
+// sdst + j * 16 KB), bank-conflict free through the swizzle; the caller bulk-stores it.
+__device__ __forceinline__ void epi_relu_image_smem(uint32_t trow, int r, int c0, int ncols,
+                                                    int n0, const float* bias, uint32_t sdst) {
+  for (int cc = 0; cc < ncols / 64; ++cc) {
+    float v[64];
+    tmem_ld32(trow + c0 + 64 * cc, *reinterpret_cast<float(*)[32]>(v));
+    tmem_ld32(trow + c0 + 64 * cc + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+    tmem_wait_ld();
+    const int n = n0 + 64 * cc;
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + bias[n + i], 0.f);
+    const uint32_t dst = sdst + (uint32_t)cc * kTile;
+#pragma unroll
+    for (int p = 0; p < 8; ++p)
+      st_shared_v4(dst + swz(r, p), pack_h2(v[8 * p], v[8 * p + 1]), pack_h2(v[8 * p + 2], v[8 * p + 3]),
+                   pack_h2(v[8 * p + 4], v[8 * p + 5]), pack_h2(v[8 * p + 6], v[8 * p + 7]));
+  }
+}
+
+// head2 epilogue: the logits of row r (TMEM columns [0, A)) + bias, this thread's half h of
+// the classes, then the selection rule; the 256 epilogue threads exchange per-row partials
+// through xch ([4][2][128] words, bar.sync 1, 256).
+// noise_col >= 0: the Gumbel noise of the row's classes was precomputed into TMEM columns
+// noise_col + class (fused tail); otherwise it is hashed here.
+__device__ __forceinline__ void epi_select(uint32_t trow, int r, int h, int stream,
+                                        const SelectArgs& g, float* xch, int noise_col = -1) {
+  const int HALF = g.A / 2;
+  const uint32_t prefix = noise_prefix(g.seed, (uint32_t)(g.stream_offset + stream), (uint32_t)g.t);
+  const int cbase = h * HALF;
+  float* lrow = g.logits ? g.logits + (size_t)stream * g.A : nullptr;
+  float best = -INFINITY, mx = -INFINITY;
+  int bi = g.A;
+#pragma unroll 1
+  for (int cc = 0; cc < HALF / 32; ++cc) {
+    float v[32], gn[32];
+    tmem_ld32(trow + cbase + 32 * cc, v);
+    if (noise_col >= 0 && g.mode == FW_SAMPLE_GUMBEL) tmem_ld32(trow + noise_col + cbase + 32 * cc, gn);
+    tmem_wait_ld();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int col = cbase + 32 * cc + i;
+      v[i] += __ldg(g.bias + col);
+      mx = fmaxf(mx, v[i]);
+      float sc = v[i];
+      if (g.mode == FW_SAMPLE_GUMBEL)
+        sc = v[i] + (noise_col >= 0 ? gn[i] : gumbel_noise(prefix, col));
+      if (sc > best) {
+        best = sc;
+        bi = col;
+      }
+    }
+    if (lrow) {
+      float4* d4 = reinterpret_cast<float4*>(lrow + cbase + 32 * cc);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+    }
+  }
+  float* xb = xch;                              // best score  [2][128]
+  int* xi = reinterpret_cast<int*>(xch + 256);  // best index [2][128]
+  float* xm = xch + 512;                        // max [2][128]
+  float* xs = xch + 768;                        // sum [2][128]
+  xb[h * 128 + r] = best;
+  xi[h * 128 + r] = bi;
+  xm[h * 128 + r] = mx;
+  named_bar_sync(1, 256);
+  int choice;
+  if (g.mode != FW_SAMPLE_INVCDF) {
+    const float ob = xb[(h ^ 1) * 128 + r];
+    const int oi = xi[(h ^ 1) * 128 + r];
+    choice = (ob > best || (ob == best && oi < bi)) ? oi : bi;
+  } else {
+    const float m = fmaxf(mx, xm[(h ^ 1) * 128 + r]);
+    float part = 0.f;
+    for (int cc = 0; cc < HALF / 32; ++cc) {
+      float v[32];
+      tmem_ld32(trow + cbase + 32 * cc, v);
+      tmem_wait_ld();
+      for (int i = 0; i < 32; ++i) part += __expf(v[i] + __ldg(g.bias + cbase + 32 * cc + i) - m);
+    }
+    xs[h * 128 + r] = part;
+    named_bar_sync(1, 256);
+    const float s0 = xs[r], total = s0 + xs[128 + r];
+    const float thr = noise_uniform(prefix, kUniformClass) * total;
+    float run = (h == 0) ? 0.f : s0;
+    int found = g.A;
+    // warp-uniform trip count: tcgen05.ld is .sync.aligned across the warp
+    for (int cc = 0; cc < HALF / 32; ++cc) {
+      float v[32];
+      tmem_ld32(trow + cbase + 32 * cc, v);
+      tmem_wait_ld();
+      for (int i = 0; i < 32; ++i) {
+        run += __expf(v[i] + __ldg(g.bias + cbase + 32 * cc + i) - m);
+        if (found == g.A && run > thr) found = cbase + 32 * cc + i;
+      }
+    }
+    xi[h * 128 + r] = found;
+    named_bar_sync(1, 256);
+    const int f0 = xi[r], f1 = xi[128 + r];
+    choice = f0 < g.A ? f0 : (f1 < g.A ? f1 : g.A - 1);
+  }
+  if (h == 0) {
+    g.out_cls[stream] = choice;
+    g.cls_next[stream] = g.next_inputs ? g.next_inputs[stream] : choice;
+  }
+}
+
 #include "chain_tc.cuh"
 
 // ---- generic [128 x BN] tile GEMM over pre-swizzled A/B images ----------------------
@@ -171,15 +336,7 @@ struct GemmArgs {
   const float* bias;  // [N]
   uint8_t* out_img;   // epi 0: [mtiles][N/64][16 KB]
   int n_total;
-  // epi 1 (head2 + selection)
-  float* logits;  // [B][A] for this step or null
-  int32_t* out_cls;
-  int32_t* cls_next;
-  const int32_t* next_inputs;  // teacher row for the next step or null
-  int B, A, mode;
-  uint32_t seed;
-  int64_t stream_offset;
-  int64_t t;
+  SelectArgs sel;  // epi 1 (head2 + selection)
 };
 
 // Each pipeline stage holds kGemmGroup consecutive 64-K chunks of A and of B, each side
@@ -199,11 +356,6 @@ constexpr uint32_t gemm_stage_bytes() {
 template <int BN>
 constexpr size_t gemm_smem() {
   return 1024 + gemm_stages<BN>() * gemm_stage_bytes<BN>() + 256 + 4 * 128 * 4 * 2;
-}
-
-__device__ __forceinline__ float gumbel_score(float v, uint32_t prefix, int cls) {
-  const float u = noise_uniform(prefix, (uint32_t)cls);
-  return v - __logf(-__logf(u));
 }
 
 template <int BN, int EPI>
@@ -280,104 +432,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) gemm_kernel(GemmArgs g) {
     mbar_wait(acc_full, 0);
     tc_fence_after();
     constexpr int HALF = BN / 2;  // columns per thread
-    if (EPI == 0) {
-      // v = ReLU(acc + bias) -> bf16 image chunk (mt, (nt*BN + h*HALF)/64 ...)
-#pragma unroll
-      for (int cc = 0; cc < HALF / 64; ++cc) {
-        float v[64];
-        tmem_ld32(trow + h * HALF + 64 * cc, *reinterpret_cast<float(*)[32]>(v));
-        tmem_ld32(trow + h * HALF + 64 * cc + 32, *reinterpret_cast<float(*)[32]>(v + 32));
-        tmem_wait_ld();
-        const int n0 = nt * BN + h * HALF + 64 * cc;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + __ldg(g.bias + n0 + i), 0.f);
-        uint8_t* dst = g.out_img + ((size_t)mt * (g.n_total / 64) + n0 / 64) * kTile;
-#pragma unroll
-        for (int p = 0; p < 8; ++p)
-          *reinterpret_cast<uint4*>(dst + swz(r, p)) =
-              make_uint4(pack_h2(v[8 * p], v[8 * p + 1]), pack_h2(v[8 * p + 2], v[8 * p + 3]),
-                         pack_h2(v[8 * p + 4], v[8 * p + 5]), pack_h2(v[8 * p + 6], v[8 * p + 7]));
-      }
-    } else {
-      // head2 + selection; this thread owns columns [h*HALF, (h+1)*HALF) of row r
-      const int stream = mt * 128 + r;
-      const uint32_t prefix =
-          noise_prefix(g.seed, (uint32_t)(g.stream_offset + stream), (uint32_t)g.t);
-      const int cbase = h * HALF;
-      float* lrow = g.logits ? g.logits + (size_t)stream * g.A : nullptr;
-      float best = -INFINITY, mx = -INFINITY;
-      int bi = g.A;
-#pragma unroll 1
-      for (int cc = 0; cc < HALF / 32; ++cc) {
-        float v[32];
-        tmem_ld32(trow + cbase + 32 * cc, v);
-        tmem_wait_ld();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int col = cbase + 32 * cc + i;
-          v[i] += __ldg(g.bias + col);
-          mx = fmaxf(mx, v[i]);
-          float sc = v[i];
-          if (g.mode == FW_SAMPLE_GUMBEL) sc = gumbel_score(v[i], prefix, col);
-          if (sc > best) {
-            best = sc;
-            bi = col;
-          }
-        }
-        if (lrow) {
-          float4* d4 = reinterpret_cast<float4*>(lrow + cbase + 32 * cc);
-#pragma unroll
-          for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-        }
-      }
-      float* xb = xch;              // best score  [2][128]
-      int* xi = reinterpret_cast<int*>(xch + 256);  // best index [2][128]
-      float* xm = xch + 512;        // max [2][128]
-      float* xs = xch + 768;        // sum [2][128]
-      xb[h * 128 + r] = best;
-      xi[h * 128 + r] = bi;
-      xm[h * 128 + r] = mx;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      int choice;
-      if (g.mode != FW_SAMPLE_INVCDF) {
-        const float ob = xb[(h ^ 1) * 128 + r];
-        const int oi = xi[(h ^ 1) * 128 + r];
-        choice = (ob > best || (ob == best && oi < bi)) ? oi : bi;
-      } else {
-        const float m = fmaxf(mx, xm[(h ^ 1) * 128 + r]);
-        float part = 0.f;
-        for (int cc = 0; cc < HALF / 32; ++cc) {
-          float v[32];
-          tmem_ld32(trow + cbase + 32 * cc, v);
-          tmem_wait_ld();
-          for (int i = 0; i < 32; ++i) part += __expf(v[i] + __ldg(g.bias + cbase + 32 * cc + i) - m);
-        }
-        xs[h * 128 + r] = part;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        const float s0 = xs[r], total = s0 + xs[128 + r];
-        const float thr = noise_uniform(prefix, kUniformClass) * total;
-        float run = (h == 0) ? 0.f : s0;
-        int found = g.A;
-        // warp-uniform trip count: tcgen05.ld is .sync.aligned across the warp
-        for (int cc = 0; cc < HALF / 32; ++cc) {
-          float v[32];
-          tmem_ld32(trow + cbase + 32 * cc, v);
-          tmem_wait_ld();
-          for (int i = 0; i < 32; ++i) {
-            run += __expf(v[i] + __ldg(g.bias + cbase + 32 * cc + i) - m);
-            if (found == g.A && run > thr) found = cbase + 32 * cc + i;
-          }
-        }
-        xi[h * 128 + r] = found;
-        asm volatile("bar.sync 1, 256;" ::: "memory");
-        const int f0 = xi[r], f1 = xi[128 + r];
-        choice = f0 < g.A ? f0 : (f1 < g.A ? f1 : g.A - 1);
-      }
-      if (h == 0) {
-        g.out_cls[stream] = choice;
-        g.cls_next[stream] = g.next_inputs ? g.next_inputs[stream] : choice;
-      }
-    }
+    if (EPI == 0)
+      epi_relu_image(trow, r, h * HALF, HALF, nt * BN + h * HALF, g.bias,
+                     g.out_img + (size_t)mt * (g.n_total / 64) * kTile);
+    else
+      epi_select(trow, r, h, mt * 128 + r, g.sel, xch);
   }
   tc_fence_before();
   __syncthreads();
@@ -520,7 +579,18 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
           pack_image(img.data() + (((size_t)e * L + l) * 2 + c) * SK * 128, SK, c * 64,
                      [&](int n, int k) { return desc->skip_w[((size_t)l * S + e * SK + n) * kD + k]; });
     if (int rc = upload_bytes(&tc->wskip2, img)) return rc;
-    if (int rc = dev_alloc(&tc->zflag, sizeof(uint32_t) * (h.batch / 128))) return rc;
+    if (int rc = dev_alloc(&tc->zflag, sizeof(uint32_t) * 3 * (h.batch / 128))) return rc;
+    // fused heads: head1's N split over the pair's nsk skip blocks, 128 or 256 columns each
+    const int nsk = S / SK, n1 = H / nsk;
+    tc->heads = tc->fused && (H % nsk == 0) && (n1 == 128 || n1 == 256);
+    if (tc->heads) {
+      std::vector<uint8_t> w1((size_t)nsk * (S / 64) * n1 * 128);
+      for (int e = 0; e < nsk; ++e)
+        for (int c = 0; c < S / 64; ++c)
+          pack_image(w1.data() + ((size_t)e * (S / 64) + c) * n1 * 128, n1, c * 64,
+                     [&](int n, int k) { return desc->head1_w[(size_t)(e * n1 + n) * S + k]; });
+      if (int rc = upload_bytes(&tc->wh1b, w1)) return rc;
+    }
   }
   {
     std::vector<uint8_t> img((size_t)(H / 128) * (S / 64) * kTile);
@@ -561,7 +631,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
 void tc_destroy(Handle& h) {
   TcState* tc = h.tc;
   if (!tc) return;
-  void* ptrs[] = {tc->wchain, tc->wskip, tc->wskip2, tc->zflag, tc->wh1, tc->wh2, tc->skip_bsum,
+  void* ptrs[] = {tc->wchain, tc->wskip, tc->wskip2, tc->zflag, tc->wh1b, tc->wh1, tc->wh2, tc->skip_bsum,
                   tc->zimg, tc->simg, tc->himg, tc->cls};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -589,6 +659,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.has_dil_bias = tc->has_dil_bias;
   ca.has_res_bias = tc->has_res_bias;
   ca.trace = tc->trace;
+  const int npairs_all = B / 128;
   ca.nchain = B / kChainRows;
   ca.zflag = tc->fused ? tc->zflag : nullptr;
   ca.wskip2 = tc->wskip2;
@@ -596,6 +667,14 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.simg = tc->simg;
   ca.S = S;
   ca.SK = tc->SK;
+  ca.heads = tc->heads;
+  ca.H = H;
+  ca.sflag = tc->zflag + npairs_all;
+  ca.hflag = tc->zflag + 2 * npairs_all;
+  ca.wh1b = tc->wh1b;
+  ca.wh2 = tc->wh2;
+  ca.h1_b = h.w.h1_b;
+  ca.himg = tc->himg;
   const int grid = tc->fused ? tc->nchain + tc->nskip : tc->nchain;
   void* kargs[] = {&ca};
   std::vector<int64_t> qoff(L);
@@ -622,20 +701,27 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   h2.a = tc->himg;
   h2.b = tc->wh2;
   h2.kch = H / 64;
-  h2.bias = h.w.h2_b;
-  h2.B = B;
-  h2.A = d.A;
-  h2.mode = run.mode;
-  h2.seed = run.seed;
-  h2.stream_offset = run.stream_offset;
-  h2.cls_next = tc->cls;
+  SelectArgs sel{};
+  sel.bias = h.w.h2_b;
+  sel.A = d.A;
+  sel.mode = run.mode;
+  sel.seed = run.seed;
+  sel.stream_offset = run.stream_offset;
+  sel.cls_next = tc->cls;
   const dim3 gskip(tc->ntile, S / 128), gh1(tc->ntile, H / 128), gh2(tc->ntile, 1);
   const int timed = h.timing ? timing_reserve(h, run.n_steps) : 0;
+  const int npairs = B / 128;
   for (int i = 0; i < run.n_steps; ++i) {
     for (int l = 0; l < L; ++l)
       ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)(B / kChainRows) * kSlotBytes;
-    if (tc->fused) {
-      cudaError_t me = cudaMemsetAsync(tc->zflag, 0, sizeof(uint32_t) * (B / 128), st);
+    sel.t = run.t0 + i;
+    sel.logits = (run.logits && i < run.n_logit_steps) ? run.logits + (size_t)i * B * d.A : nullptr;
+    sel.out_cls = run.out + (size_t)i * B;
+    sel.next_inputs = (i + 1 < run.n_inputs) ? run.inputs + (size_t)(i + 1) * B : nullptr;
+    h2.sel = sel;
+    ca.sel = sel;
+    if (tc->fused) {  // zflag | sflag | hflag of every tile pair restart at 0 each step
+      cudaError_t me = cudaMemsetAsync(tc->zflag, 0, sizeof(uint32_t) * 3 * npairs, st);
       if (me != cudaSuccess) return me;
     }
     if (i < timed) cudaEventRecord(h.tev[3 * i], st);
@@ -648,16 +734,14 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
     }
     if (i < timed) cudaEventRecord(h.tev[3 * i + 1], st);
     if (!tc->fused) gemm_kernel<128, 0><<<gskip, kGemmThreads, gemm_smem<128>(), st>>>(skip);
-    gemm_kernel<128, 0><<<gh1, kGemmThreads, gemm_smem<128>(), st>>>(h1);
-    h2.t = run.t0 + i;
-    h2.logits = (run.logits && i < run.n_logit_steps) ? run.logits + (size_t)i * B * d.A : nullptr;
-    h2.out_cls = run.out + (size_t)i * B;
-    h2.next_inputs = (i + 1 < run.n_inputs) ? run.inputs + (size_t)(i + 1) * B : nullptr;
-    gemm_kernel<256, 1><<<gh2, kGemmThreads, gemm_smem<256>(), st>>>(h2);
+    if (!tc->heads) {
+      gemm_kernel<128, 0><<<gh1, kGemmThreads, gemm_smem<128>(), st>>>(h1);
+      gemm_kernel<256, 1><<<gh2, kGemmThreads, gemm_smem<256>(), st>>>(h2);
+    }
     if (i < timed) cudaEventRecord(h.tev[3 * i + 2], st);
   }
   h.tev_used = timed;
-  *launches = (tc->fused ? 3 : 4) * (int64_t)run.n_steps;
+  *launches = (tc->heads ? 1 : tc->fused ? 3 : 4) * (int64_t)run.n_steps;
   return cudaGetLastError();
 }
 

@@ -59,10 +59,14 @@ constexpr uint32_t kSlotBytes = 16384;  // one tile's ring slot: [16 K-pieces][6
 constexpr uint32_t kStageA = 32768, kStageB = 65536, kStageC = 32768;
 constexpr uint32_t kOffA0 = 0, kOffA1 = kOffA0 + kStageA, kOffB = kOffA1 + kStageA,
                    kOffC = kOffB + kStageB, kOffBars = kOffC + kStageC;
-// skip role: a 2-stage ring of (z tile 32 KB | W_skip block SK x 128 x 2 B, <= 64 KB)
+// skip role: a 2-stage ring of (z tile 32 KB | W_skip block SK x 128 x 2 B, <= 64 KB), later
+// reused by the fused heads as a 4-stage ring of (A chunk 16 KB | B chunk <= 256 x 128 B);
+// then barriers and the selection exchange buffer (4 KB)
 constexpr uint32_t kSkipStage = 2 * kTile + 65536;
 constexpr uint32_t kSkipBars = 2 * kSkipStage;
-constexpr size_t kChainSmem = 1024 + (kOffBars > kSkipBars ? kOffBars : kSkipBars) + 256;
+constexpr uint32_t kTailStage = 2 * (kTile + 32768);  // 2 K-chunks of A | 2 of B (N <= 256)
+constexpr int kTailStages = 2;
+constexpr size_t kChainSmem = 1024 + (kOffBars > kSkipBars ? kOffBars : kSkipBars) + 256 + 4096 + 4096;
 
 // z stash row base of (tile, layer): [tile pair][L][16 pieces][128 rows][16 B]
 __device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int L, int l) {
@@ -74,6 +78,8 @@ __device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int L, in
 // one SK-column block of S, accumulated in TMEM layer by layer as the chain CTAs stash z_l
 // (a per-pair counter in global memory, +1 per chain tile per layer). Runs on SMs the chain
 // leaves idle, so the skip GEMM costs no time after the chain ends.
+// With fused heads the pair's blocks then run head1 (H / nsk columns each, once every block
+// of the pair has published its part of s) and block 0 head2 + the selection rule.
 __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int k) {
   const int SK = a.SK, nsk = a.S / SK;
   const int p = k / nsk, e = k % nsk;
@@ -84,78 +90,219 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
   uint64_t* empty = bars + 2;  // [2]
   uint64_t* acc_full = bars + 4;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 5);
+  uint64_t* tfull = bars + 6;    // [4] fused heads ring
+  uint64_t* tempty = bars + 10;  // [4]
+  uint64_t* tacc = bars + 14;    // head1 (phase 0) / head2 (phase 1) accumulator complete
+  uint64_t* tfree = bars + 15;   // 256: epilogue done reading TMEM (phase 0 s, 1 h)
+  uint64_t* noise_ready = bars + 16;  // 128: Gumbel noise in TMEM [256,512)
+  float* xch = reinterpret_cast<float*>(smem + kSkipBars + 256);
+  // biases of this block's epilogues, staged while the chain runs: skip [0,SK), head1 [SK, SK+n1)
+  float* sbias = reinterpret_cast<float*>(smem + kSkipBars + 256 + 4096);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.S, H = a.H, n1 = a.H / nsk;
+  const bool heads = a.heads != 0, sel_block = heads && e == 0;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < 5; ++i) mbar_init(bars + i, 1);
+    for (int i = 0; i < 15; ++i) mbar_init(bars + i, (i >= 6 && i < 10) ? 2 : 1);  // tfull: 2 producers
+    mbar_init(tfree, 256);
+    mbar_init(noise_ready, 128);
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc(tmem_holder, 256);
+  // TMEM: accumulator (s, then h, then the logits) at [0,256); the selecting block keeps the
+  // step's Gumbel noise of its 128 streams x 256 classes at [256,512), computed by warps
+  // 10..13 while the chain runs
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  const int k1 = S / 64, k2 = H / 64;  // K-chunks of head1 / head2
+  // fused heads' operand stream: 2 K-chunks per stage; A (the s / h images) by warp 0, B (the
+  // W1 / W2 chunks) by warp 11 -- the copy engine's cost is per operation and a thread's
+  // copies run one after another (tools/ring_bw.cu)
+  auto tail_loads = [&](bool is_b) {
+    const uint32_t b1 = (uint32_t)n1 * 128, b2 = (uint32_t)a.sel.A * 128;
+    const int it1 = k1 / 2, it2 = sel_block ? k2 / 2 : 0;
+    for (int it = 0; it < it1 + it2; ++it) {
+      const int st = it % kTailStages;
+      mbar_wait(tempty + st, ((uint32_t)(it / kTailStages) & 1) ^ 1);
+      if (it == 0) {
+        wait_counter(a.sflag + p, (uint32_t)nsk);
+        fence_proxy_async_all();
+      }
+      if (it == it1) {
+        wait_counter(a.hflag + p, (uint32_t)nsk);
+        fence_proxy_async_all();
+      }
+      const bool two = it >= it1;
+      const int c = two ? 2 * (it - it1) : 2 * it;
+      const uint32_t bb = two ? b2 : b1;
+      uint8_t* stage = smem + st * kTailStage;
+      if (!is_b) {
+        mbar_arrive_expect_tx(tfull + st, 2 * kTile);
+        const uint8_t* src = two ? a.himg + ((size_t)p * k2 + c) * kTile
+                                 : a.simg + ((size_t)p * k1 + c) * kTile;
+        bulk_g2s(stage, src, 2 * kTile, tfull + st);
+      } else {
+        const uint8_t* src = two ? a.wh2 + (size_t)c * b2 : a.wh1b + ((size_t)e * k1 + c) * b1;
+        mbar_arrive_expect_tx(tfull + st, 2 * bb);
+        bulk_g2s(stage + 2 * kTile, src, 2 * bb, tfull + st);
+      }
+    }
+  };
   if (warp == 0) {
     if (lane == 0) {  // producer: z tile of (p, l) once both chain tiles stashed it
       for (int l = 0; l < L; ++l) {
         const int st = l & 1;
         mbar_wait(empty + st, ((uint32_t)(l >> 1) & 1) ^ 1);
         wait_counter(a.zflag + p, 2u * (uint32_t)(l + 1));
+        if (l == L - 1) trace_g(a, k == 0, 2);
         fence_proxy_async_all();
         uint8_t* stage = smem + st * kSkipStage;
         mbar_arrive_expect_tx(full + st, 2 * kTile + bbytes);
         bulk_g2s(stage, a.zimg + ((size_t)p * L + l) * 2 * kTile, 2 * kTile, full + st);
         bulk_g2s(stage + 2 * kTile, a.wskip2 + ((size_t)e * L + l) * bbytes, bbytes, full + st);
       }
+      if (heads) tail_loads(false);
     }
   } else if (warp == 1) {
-    const uint32_t id = idesc_f16(128, SK);
     const uint32_t s0 = smem_u32(smem);
-    for (int l = 0; l < L; ++l) {
-      const int st = l & 1;
-      mbar_wait(full + st, (uint32_t)(l >> 1) & 1);
-      tc_fence_after();
-      const uint32_t sa = s0 + st * kSkipStage, sb = sa + 2 * kTile;
-      if (elect_one()) {
+    {
+      const uint32_t id = idesc_f16(128, SK);
+      for (int l = 0; l < L; ++l) {
+        const int st = l & 1;
+        mbar_wait(full + st, (uint32_t)(l >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sa = s0 + st * kSkipStage, sb = sa + 2 * kTile;
+        if (elect_one()) {
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+          for (int c = 0; c < 2; ++c)
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            mma_bf16(tmem, sdesc_plain(sa + c * kTile + kk * 4096, 2048, 128),
-                     sdesc_sw128(sb + c * (uint32_t)SK * 128 + kk * 32), id, (l | c | kk) != 0);
-        mma_commit(empty + st);
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16(tmem, sdesc_plain(sa + c * kTile + kk * 4096, 2048, 128),
+                       sdesc_sw128(sb + c * (uint32_t)SK * 128 + kk * 32), id, (l | c | kk) != 0);
+          mma_commit(empty + st);
+        }
+        __syncwarp();
       }
+      if (elect_one()) mma_commit(acc_full);
       __syncwarp();
+      trace_g(a, k == 0 && lane == 0, 7);
     }
-    if (elect_one()) mma_commit(acc_full);
-    __syncwarp();
+    if (heads) {
+      const int it1 = k1 / 2;
+      for (int g = 0; g < (sel_block ? 2 : 1); ++g) {
+        const int nb = g == 0 ? n1 : a.sel.A;
+        const uint32_t id = idesc_f16(128, nb);
+        mbar_wait(tfree, (uint32_t)g);  // the epilogue has read the previous accumulator
+        tc_fence_after();
+        trace_g(a, k == 0 && lane == 0, 8 + 3 * g);
+        const int i0 = g == 0 ? 0 : it1, ni = g == 0 ? it1 : k2 / 2;
+        for (int it = i0; it < i0 + ni; ++it) {
+          const int st = it % kTailStages;
+          mbar_wait(tfull + st, (uint32_t)(it / kTailStages) & 1);
+          tc_fence_after();
+          const uint32_t sa = s0 + st * kTailStage, sb = sa + 2 * kTile;
+          if (it == i0) trace_g(a, k == 0 && lane == 0, 9 + 3 * g);
+          if (elect_one()) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int kk = 0; kk < 4; ++kk)
+                mma_bf16(tmem, sdesc_sw128(sa + c * kTile + kk * 32),
+                         sdesc_sw128(sb + c * (uint32_t)nb * 128 + kk * 32), id,
+                         (it > i0 || c || kk) ? 1u : 0u);
+            mma_commit(tempty + st);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit(tacc);
+        __syncwarp();
+        trace_g(a, k == 0 && lane == 0, 10 + 3 * g);
+      }
+    }
   } else if (warp >= 2 && warp < 10) {
-    // epilogue: row r, columns [h*SK/2, (h+1)*SK/2) -> bias + ReLU -> head1's A image
+    // epilogue: row r, columns [h*cols/2, (h+1)*cols/2) of the accumulator
     const int sub = warp & 3, h = (warp - 2) >> 2;
     const int r = sub * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
+    for (int i = threadIdx.x - 64; i < SK + (heads ? n1 : 0); i += 256)
+      sbias[i] = i < SK ? a.skip_bsum[e * SK + i] : a.h1_b[e * n1 + (i - SK)];
+    named_bar_sync(1, 256);
     mbar_wait(acc_full, 0);
     tc_fence_after();
-    const int half = SK / 2;
-    for (int cc = 0; cc < half / 64; ++cc) {
-      float v[64];
-      tmem_ld32(trow + h * half + 64 * cc, *reinterpret_cast<float(*)[32]>(v));
-      tmem_ld32(trow + h * half + 64 * cc + 32, *reinterpret_cast<float(*)[32]>(v + 32));
-      tmem_wait_ld();
-      const int n0 = e * SK + h * half + 64 * cc;
-#pragma unroll
-      for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + __ldg(a.skip_bsum + n0 + i), 0.f);
-      uint8_t* dst = a.simg + ((size_t)p * (a.S / 64) + n0 / 64) * kTile;
-#pragma unroll
-      for (int pp = 0; pp < 8; ++pp)
-        *reinterpret_cast<uint4*>(dst + swz(r, pp)) =
-            make_uint4(pack_h2(v[8 * pp], v[8 * pp + 1]), pack_h2(v[8 * pp + 2], v[8 * pp + 3]),
-                       pack_h2(v[8 * pp + 4], v[8 * pp + 5]), pack_h2(v[8 * pp + 6], v[8 * pp + 7]));
+    trace_g(a, k == 0 && warp == 2 && lane == 0, 14);
+    // ReLU(s + bias) -> this block's SK/64 chunks of the pair's s images: staged in shared
+    // memory (the tail ring is idle now) and written with one bulk store -- per-thread
+    // 16-byte stores of swizzled rows would touch 32 lines per warp instruction
+    const uint32_t stg = smem_u32(smem);
+    epi_relu_image_smem(trow, r, h * (SK / 2), SK / 2, h * (SK / 2), sbias, stg + h * (SK / 128) * kTile);
+    fence_proxy_async();
+    tc_fence_before();
+    if (heads) mbar_arrive(tfree);  // s read out of TMEM
+    named_bar_sync(1, 256);
+    if (warp == 2 && lane == 0) {
+      bulk_s2g(a.simg + ((size_t)p * (S / 64) + e * SK / 64) * kTile, smem, (uint32_t)SK * 256);
+      bulk_commit();
+      bulk_wait0();
+      fence_proxy_async_all();
+      if (heads) red_release_gpu(a.sflag + p, 1u);
+      trace_g(a, k == 0, 3);
     }
+    if (heads) {
+      // head1 part: h columns [e*n1, (e+1)*n1) -> the pair's h images
+      mbar_wait(tacc, 0);
+      tc_fence_after();
+      trace_g(a, k == 0 && warp == 2 && lane == 0, 15);
+      // the tail ring holds no live operands once head1's accumulator is complete
+      named_bar_sync(1, 256);
+      epi_relu_image_smem(trow, r, h * (n1 / 2), n1 / 2, h * (n1 / 2), sbias + SK,
+                          stg + h * (n1 / 128) * kTile);
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(tfree);
+      named_bar_sync(1, 256);
+      if (warp == 2 && lane == 0) {
+        bulk_s2g(a.himg + ((size_t)p * (H / 64) + e * n1 / 64) * kTile, smem, (uint32_t)n1 * 256);
+        bulk_commit();
+        bulk_wait0();
+        fence_proxy_async_all();
+        red_release_gpu(a.hflag + p, 1u);
+        trace_g(a, k == 0, 4);
+      }
+      if (sel_block) {  // head2 logits + the selection rule for the pair's 128 streams
+        mbar_wait(tacc, 1);
+        if (a.sel.mode == FW_SAMPLE_GUMBEL) mbar_wait(noise_ready, 0);
+        tc_fence_after();
+        trace_g(a, k == 0 && warp == 2 && lane == 0, 5);
+        epi_select(trow, r, h, p * 128 + r, a.sel, xch, 256);
+        trace_g(a, k == 0 && warp == 2 && lane == 0, 6);
+      }
+    }
+  } else if (warp >= 10 && warp < 14) {
+    if (sel_block && a.sel.mode == FW_SAMPLE_GUMBEL) {
+      // the step's Gumbel noise of row r (stream p*128 + r), 256 classes -> TMEM [256,512)
+      const int sub = warp & 3;
+      const int r = sub * 32 + lane;
+      const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
+      const uint32_t prefix = noise_prefix(a.sel.seed, (uint32_t)(a.sel.stream_offset + p * 128 + r),
+                                           (uint32_t)a.sel.t);
+#pragma unroll 1
+      for (int cc = 0; cc < 8; ++cc) {
+        float gn[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) gn[i] = gumbel_noise(prefix, 32 * cc + i);
+        tmem_st32(trow + 256 + 32 * cc, gn);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(noise_ready);
+    }
+    if (warp == 11 && lane == 0 && heads) tail_loads(true);
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc(tmem, 256);
+  if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
 // One launch per step: blocks [0, nchain) run the chain of one 64-stream tile each, blocks
@@ -464,6 +611,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       const uint32_t o = __shfl_xor_sync(0xffffffffu, w, 2);
       return pc == 0 ? __byte_perm(w, o, 0x5410) : __byte_perm(o, w, 0x7632);
     };
+    trace_g(a, tr, 0);
     for (int l = 0; l < L; ++l) {
       const uint32_t par = (uint32_t)l & 1;
       if (tr) trace_at(a, l, T_EPI_A, clock64());
@@ -543,6 +691,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         if (tr) trace_at(a, l, hh == 0 ? T_EPI_Z0 : T_EPI_Z1, clock64());
       }
     }
+    trace_g(a, tr, 1);
   }
   tc_fence_before();
   __syncthreads();

@@ -125,6 +125,12 @@ __device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t target)
   }
 }
 
+__device__ __forceinline__ long long globaltimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 // One lane of a converged warp (the warp's leader). tcgen05.mma issued under elect.sync from
 // a converged warp runs back to back; issued from a lone divergent thread, ptxas wraps every
 // MMA in an ELECT loop and the tensor pipe sees ~95-115 cycles per M=128 MMA instead of

@@ -8,7 +8,8 @@
 
 using namespace fw::ptx;
 
-__global__ void probe(int k, int ts, long long* out) {
+// pre > 0: the timed burst follows `pre` untimed MMAs into another accumulator (busy pipe)
+__global__ void probe(int k, int ts, long long* out, int pre) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar, go;
   __shared__ uint32_t holder;
@@ -34,6 +35,12 @@ __global__ void probe(int k, int ts, long long* out) {
     if (warp == 0) {
       // let the waiter park on the barrier first
       __nanosleep(2000);
+      if (pre > 0) {
+        if (elect_one())
+          for (int i = 0; i < pre; ++i)
+            mma_bf16_ta(tmem + 256, tmem + 448 + (i & 7) * 8, sdesc_sw128(sb + (i & 3) * 32), id, 1u);
+        __syncwarp();
+      }
       const long long t0 = clock64();
       if (elect_one()) {
         for (int i = 0; i < k; ++i) {
@@ -79,15 +86,16 @@ int main() {
   long long* d;
   cudaMalloc(&d, 128);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 + 1024);
-  for (int ts = 0; ts < 2; ++ts)
-    for (int k : {1, 2, 4, 8, 16}) {
-      probe<<<1, 64, 32768 + 1024>>>(k, ts, d);
-      probe<<<1, 64, 32768 + 1024>>>(k, ts, d);
+  for (int pre : {0, 2, 16})
+  for (int ts = 1; ts < 2; ++ts)
+    for (int k : {1, 4, 8}) {
+      probe<<<1, 64, 32768 + 1024>>>(k, ts, d, pre);
+      probe<<<1, 64, 32768 + 1024>>>(k, ts, d, pre);
       long long h[3] = {0, 0, 0};
       cudaError_t e = cudaDeviceSynchronize();
       cudaMemcpy(h, d, 24, cudaMemcpyDeviceToHost);
-      printf("%s k=%2d N=128: issue %5lld, done (issuer) %5lld, done (other warp) %5lld cycles %s\n",
-             ts ? "TS" : "SS", k, h[0], h[1], h[2], e ? cudaGetErrorString(e) : "");
+      printf("pre %2d %s k=%2d N=128: issue %5lld, done (issuer) %5lld, done (other warp) %5lld cycles %s\n",
+             pre, ts ? "TS" : "SS", k, h[0], h[1], h[2], e ? cudaGetErrorString(e) : "");
     }
   return 0;
 }

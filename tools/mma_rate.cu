@@ -10,7 +10,7 @@ using namespace fw::ptx;
 
 // rot >= 8: elect-issued; bit 16 of rot: random operand data; bit 17: 4 extra warps stream
 // tcgen05.ld from TMEM columns 256..447 while the MMAs run
-__global__ void probe(int n, int ts, int count, long long* out, int rot) {
+__global__ void probe(int n, int ts, int count, long long* out, int rot, int mrows) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t holder;
@@ -48,7 +48,7 @@ __global__ void probe(int n, int ts, int count, long long* out, int rot) {
     if (acc == 0x12345678u) out[2] = acc;
   }
   if (elect_mode ? warp == 0 : threadIdx.x == 0) {
-    const uint32_t id = idesc_f16(128, n);
+    const uint32_t id = idesc_f16(mrows, n);
     const uint32_t sa = smem_u32(smem), sb = sa + 16384;
     // warm-up
     if (!elect_mode || (threadIdx.x & 31) == 0)
@@ -112,18 +112,19 @@ int main() {
   long long* d;
   cudaMalloc(&d, 32);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
-  for (int rot : {8, 8 | 0x10000, 8 | 0x20000, 8 | 0x30000})
+  for (int mrows : {64, 128})
+  for (int rot : {8})
   for (int ts = 0; ts < 2; ++ts)
-    for (int n : {128, 256}) {
+    for (int n : {32, 64, 128, 256}) {
 
       const int count = 512;
-      probe<<<1, 256, 65536 + 1024>>>(n, ts, count, d, rot);
-      probe<<<1, 256, 65536 + 1024>>>(n, ts, count, d, rot);
+      probe<<<1, 256, 65536 + 1024>>>(n, ts, count, d, rot, mrows);
+      probe<<<1, 256, 65536 + 1024>>>(n, ts, count, d, rot, mrows);
       long long h[2] = {0, 0};
       cudaError_t e = cudaDeviceSynchronize();
       cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-      printf("mode %x %s M=128 N=%3d K=16: issue %6.1f cyc/mma, complete %6.1f cyc/mma (floor %d) %s\n",
-             rot, ts ? "TS" : "SS", n, (double)h[0] / count, (double)h[1] / count, 128 * n / 256,
+      printf("mode %x %s M=%d N=%3d K=16: issue %6.1f cyc/mma, complete %6.1f cyc/mma (floor %d) %s\n",
+             rot, ts ? "TS" : "SS", mrows, n, (double)h[0] / count, (double)h[1] / count, 128 * n / 256,
              e ? cudaGetErrorString(e) : "");
     }
   return 0;

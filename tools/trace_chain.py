@@ -37,7 +37,7 @@ def main():
     m = build_cell_model(spec.cell)
     gen = CellGenerator(m, spec.batch, kernel="tcgen05")
     L = spec.cell.total_layers
-    tr = torch.zeros((L, SLOTS), dtype=torch.int64, device="cuda")
+    tr = torch.zeros((L + 1, SLOTS), dtype=torch.int64, device="cuda")
     _lib.check(gen._lib.fw_debug_trace(gen._h, C.c_void_p(tr.data_ptr())))
     primer = torch.full((1, spec.batch), 128, dtype=torch.int32, device="cuda")
     gen.generate(primer, args.steps, Sampler(spec.sampler, configs.NOISE_SEED))
@@ -58,6 +58,16 @@ def main():
             else:
                 cells.append(f"{v - ref:8d}")
         print(f"{l:5d} " + " ".join(cells) + f"   (start {ref - base})")
+    g = t[L]
+    if g[0]:
+        names = ["chain start", "chain last layer", "skip: last z seen", "s published",
+                 "head1 published", "head2 acc seen", "selection done", "skip acc committed",
+                 "h1 mma: tmem free", "h1 first stage", "h1 acc committed",
+                 "h2 mma: tmem free", "h2 first stage", "h2 acc committed", "epi: skip acc seen",
+                 "epi: h1 acc seen"]
+        print("step timeline (global ns, last step): " + ", ".join(
+            f"{n} {(g[i] - g[0]) / 1e3:.2f} us" for i, n in enumerate(names) if g[i]))
+    t = t[:L]
     per_layer = np.diff(t[:, 8])
     print(f"mean cycles/layer {per_layer.mean():.0f}; total {t[-1, 8] - base}; "
           f"weight-wait cycles total {t[:, 7].sum()}")
