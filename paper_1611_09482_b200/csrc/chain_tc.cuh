@@ -338,6 +338,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
   uint64_t* z0_ready = bars + 15;  // 256
   uint64_t* z1_ready = bars + 16;  // 256
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
+  uint64_t* xd_free = bars + 18;   // commit: this layer's x_{t-d} MMAs are done with TMEM xd
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
@@ -351,6 +352,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     mbar_init(xt_ready, 256);
     mbar_init(z0_ready, 256);
     mbar_init(z1_ready, 256);
+    mbar_init(xd_free, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -450,7 +452,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       if (lane == 0) trace_at(a, l, T_MMA_ACC0, clock64());
       if (!early[1]) {
         wait_w(fullA1, par);
-        if (elect_one()) xd_half(1);
+        if (elect_one()) {
+          xd_half(1);
+          mma_commit(xd_free);
+        }
         __syncwarp();
       }
       early[0] = early[1] = false;
@@ -470,14 +475,16 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         wait_w(fullC, par);
         if (elect_one()) mma_tmem_a(tmem + kP1 + kColX, tmem + kP1 + kColZ + 0, sc + 0 * kChunk);
         __syncwarp();
-        // acc0 is free (gate half 0 done): layer l+1's x_{t-d} N-half 0 if its operand and
-        // weights are in place -- never wait for them here
-        if (ready(l + 1, fullA0)) {
-          tc_fence_after();
-          if (elect_one()) xd_half(0);
-          __syncwarp();
-          early[0] = true;
-        }
+        // acc0 is free (gate half 0 done): layer l+1's x_{t-d} N-half 0. Its operand follows
+        // this layer's x_{t-d} MMAs (xd_free) within a few hundred cycles and its weights
+        // loaded a layer ago, so waiting here costs little; issued after x_full instead it
+        // would sit in front of the next layer's x_t MMAs.
+        mbar_wait(xd_ready, (uint32_t)(l + 1) & 1);
+        tc_fence_after();
+        wait_w(fullA0, (uint32_t)(l + 1) & 1);
+        if (elect_one()) xd_half(0);
+        __syncwarp();
+        early[0] = true;
       }
       mbar_wait(z1_ready, par);
       if (lane == 0) trace_at(a, l, T_MMA_Z1, clock64());
@@ -500,12 +507,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
           __syncwarp();
           early[0] = true;
         }
-        if (ready(l + 1, fullA1)) {
-          tc_fence_after();
-          if (elect_one()) xd_half(1);
-          __syncwarp();
-          early[1] = true;
-        }
+        // (x_{t-d} half 1 stays in the layer: issued here it would hold the tensor pipe
+        // and this warp when the next layer's x_t MMAs become ready)
       }
       if (lane == 0) trace_at(a, l, T_MMA_WWAIT, wwait);
     }
@@ -575,9 +578,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       tc_fence_before();
       mbar_arrive(x_pushed);
       if (tq) trace_at(a, l, T_Q_LOAD, clock64());
-      // x_{t-d} of layer l+1 -> TMEM xd once layer l's x_{t-d} MMAs are done (acc1_full)
+      // x_{t-d} of layer l+1 -> TMEM xd once layer l's x_{t-d} MMAs are done (xd_free)
       if (l + 1 < L) {
-        mbar_wait(acc1_full, par);
+        mbar_wait(xd_free, par);
         tc_fence_after();
         store_xd();
         if (tq) trace_at(a, l + 1, T_Q_XD, clock64());
