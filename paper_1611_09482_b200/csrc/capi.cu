@@ -120,8 +120,7 @@ int run_cell(Handle& h, const CellRun& run, cudaStream_t st) {
   cudaError_t e;
   int64_t launches = 0;
   if (h.kernel == FW_KERNEL_TCGEN05) {
-    e = launch_cell_tc(h, run, st, &launches);
-    h.timed_steps = h.tev_used;
+    e = launch_cell_tc(h, run, st, &launches);  // sets tev_used / timed_steps
   } else {
     // one persistent launch covers every step: time it as a whole
     const int timed = h.timing ? timing_reserve(h, 1) : 0;

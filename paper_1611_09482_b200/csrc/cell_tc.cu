@@ -22,6 +22,9 @@
 // operand image of x (the precision the MMA consumes). DESIGN.md, "Numerics".
 #include <cuda_bf16.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <vector>
 
@@ -35,7 +38,8 @@ struct TcState {
   uint8_t* wchain = nullptr;  // per layer: 10 chunks [128][64] in MMA issue order
   uint8_t* wskip = nullptr;   // [S/128][L*D/64] chunks of [128][64] (unfused skip GEMM)
   uint8_t* wskip2 = nullptr;  // [S/SK][L][2][SK][64] (fused skip role of the step kernel)
-  uint32_t* zflag = nullptr;  // [B/128] z stash counters of the fused skip role
+  uint32_t* zflag = nullptr;  // [4][B/128] fused counters: z stash | s | h | selections
+  int64_t* d_qoff = nullptr;  // [L] byte offset of each layer's ring
   int fused = 0, SK = 256, nchain = 0, nskip = 0;
   int heads = 0;              // head1 / head2 fused into the skip blocks (needs fused)
   uint8_t* wh1b = nullptr;    // [nsk][S/64][H/nsk rows][128 B] (fused head1)
@@ -111,11 +115,32 @@ struct SelectArgs {
   uint32_t seed;
   int64_t stream_offset;
   int64_t t;
+  // whole-call view (the persistent step kernel derives the per-step fields above)
+  int32_t* out_base;           // [n_steps][B]
+  float* logits_base;          // [n_logit_steps][B][A] or null
+  int n_logit_steps;
+  const int32_t* inputs;       // [n_inputs][B]
+  int n_inputs, B;
 };
+
+// The per-step fields of step i of a call starting at absolute step t0.
+__device__ __forceinline__ SelectArgs sel_step(const SelectArgs& s, int64_t t0, int i) {
+  SelectArgs r = s;
+  r.t = t0 + i;
+  r.out_cls = s.out_base + (size_t)i * s.B;
+  r.logits = (s.logits_base && i < s.n_logit_steps) ? s.logits_base + (size_t)i * s.B * s.A : nullptr;
+  r.next_inputs = (i + 1 < s.n_inputs) ? s.inputs + (size_t)(i + 1) * s.B : nullptr;
+  return r;
+}
 
 struct ChainArgs {
   int B, L;
-  int64_t qbase[kMaxChainLayers];  // byte offset of slot (t mod d_l) of layer l's ring (tile 0)
+  int n_steps;             // steps of this launch (the fused kernel runs them all)
+  int64_t t0;              // absolute step index of the first one
+  int32_t dil[kMaxChainLayers];    // dilations
+  int32_t slot0[kMaxChainLayers];  // t0 mod dil[l]: the ring slot of layer l at step 0
+  const int64_t* qoff;     // [L] byte offset of layer l's ring (slot 0, tile 0)
+  int64_t slot_stride;     // bytes between ring slots (all tiles of one slot)
   uint8_t* queue;
   const uint8_t* w;
   const float* embed;  // [A][128]
@@ -127,7 +152,8 @@ struct ChainArgs {
   long long* trace;  // [L][kTraceSlots] or null
   // fused skip role (zflag != null): blocks >= nchain accumulate the skip sum
   int nchain;
-  uint32_t* zflag;         // [B/128] per tile pair: chain tiles x layers stashed this step
+  uint32_t* zflag;         // [B/128] per tile pair: chain tiles x layers stashed so far
+  uint32_t* cls_ready;     // [B/128] per tile pair: steps whose selection is written
   const uint8_t* wskip2;   // [S/SK][L][2 K-chunks][SK rows][128 B]
   const float* skip_bsum;  // [S]
   uint8_t* simg;           // head1's A images [B/128][S/64][16 KB]
@@ -135,7 +161,7 @@ struct ChainArgs {
   // fused heads (heads != 0): head1 by the pair's skip blocks (H / nsk columns each), head2
   // + selection by its first skip block; sflag / hflag count the blocks done with simg / himg
   int heads, H;
-  uint32_t* sflag;       // [B/128]
+  uint32_t* sflag;       // [B/128] (cumulative over the launch's steps)
   uint32_t* hflag;       // [B/128]
   const uint8_t* wh1b;   // [nsk][S/64][H/nsk rows][128 B]
   const uint8_t* wh2;    // [H/64][A rows][128 B]
@@ -152,6 +178,13 @@ __device__ __forceinline__ void trace_at(const ChainArgs& a, int l, int slot, lo
 // 2 skip: last z tile seen, 3 s published, 4 head1 done, 5 head2 accumulator, 6 selection done
 __device__ __forceinline__ void trace_g(const ChainArgs& a, bool who, int slot) {
   if (a.trace != nullptr && who) a.trace[a.L * kTraceSlots + slot] = globaltimer_ns();
+}
+// Byte offset (tile 0) of the ring slot layer l reads and writes at step i of the launch.
+__device__ __forceinline__ int64_t qbase_of(const ChainArgs& a, int i, int l) {
+  const int d = a.dil[l];
+  int s = a.slot0[l] + i;  // 32-bit: i < n_steps
+  s = (d & (d - 1)) == 0 ? (s & (d - 1)) : s % d;
+  return a.qoff[l] + (int64_t)s * a.slot_stride;
 }
 
 __device__ __forceinline__ void ld64(float (&v)[64], const float* p) {
@@ -579,10 +612,21 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
           pack_image(img.data() + (((size_t)e * L + l) * 2 + c) * SK * 128, SK, c * 64,
                      [&](int n, int k) { return desc->skip_w[((size_t)l * S + e * SK + n) * kD + k]; });
     if (int rc = upload_bytes(&tc->wskip2, img)) return rc;
-    if (int rc = dev_alloc(&tc->zflag, sizeof(uint32_t) * 3 * (h.batch / 128))) return rc;
+    if (int rc = dev_alloc(&tc->zflag, sizeof(uint32_t) * 4 * (h.batch / 128))) return rc;
+    // ring offsets: layer l's d_l slots follow the earlier layers', each slot holds every tile
+    std::vector<int64_t> qoff(L);
+    for (int l = 0, acc = 0; l < L; ++l) {
+      qoff[l] = (int64_t)acc * (h.batch / kChainRows) * kSlotBytes;
+      acc += h.dil[l];
+    }
+    if (int rc = dev_alloc(&tc->d_qoff, sizeof(int64_t) * L)) return rc;
+    cudaMemcpy(tc->d_qoff, qoff.data(), sizeof(int64_t) * L, cudaMemcpyHostToDevice);
     // fused heads: head1's N split over the pair's nsk skip blocks, 128 or 256 columns each
     const int nsk = S / SK, n1 = H / nsk;
+    // the fused step kernel runs all steps of a call in one launch, so it needs the heads
+    // too; other shapes keep per-step launches with the skip / head GEMM kernels
     tc->heads = tc->fused && (H % nsk == 0) && (n1 == 128 || n1 == 256);
+    tc->fused = tc->heads;
     if (tc->heads) {
       std::vector<uint8_t> w1((size_t)nsk * (S / 64) * n1 * 128);
       for (int e = 0; e < nsk; ++e)
@@ -631,7 +675,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
 void tc_destroy(Handle& h) {
   TcState* tc = h.tc;
   if (!tc) return;
-  void* ptrs[] = {tc->wchain, tc->wskip, tc->wskip2, tc->zflag, tc->wh1b, tc->wh1, tc->wh2, tc->skip_bsum,
+  void* ptrs[] = {tc->wchain, tc->wskip, tc->wskip2, tc->zflag, tc->d_qoff, tc->wh1b, tc->wh1, tc->wh2, tc->skip_bsum,
                   tc->zimg, tc->simg, tc->himg, tc->cls};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -677,11 +721,13 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.himg = tc->himg;
   const int grid = tc->fused ? tc->nchain + tc->nskip : tc->nchain;
   void* kargs[] = {&ca};
-  std::vector<int64_t> qoff(L);
-  for (int l = 0, acc = 0; l < L; ++l) {
-    qoff[l] = (int64_t)acc * (B / kChainRows) * kSlotBytes;
-    acc += h.dil[l];
+  for (int l = 0; l < L; ++l) {
+    ca.dil[l] = h.dil[l];
+    ca.slot0[l] = (int32_t)(run.t0 % h.dil[l]);
   }
+  ca.qoff = tc->d_qoff;
+  ca.slot_stride = (int64_t)(B / kChainRows) * kSlotBytes;
+  ca.cls_ready = tc->zflag + 3 * npairs_all;
   GemmArgs skip{};
   skip.a = tc->zimg;
   skip.b = tc->wskip;
@@ -708,40 +754,85 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   sel.seed = run.seed;
   sel.stream_offset = run.stream_offset;
   sel.cls_next = tc->cls;
+  sel.out_base = run.out;
+  sel.logits_base = run.logits;
+  sel.n_logit_steps = run.n_logit_steps;
+  sel.inputs = run.inputs;
+  sel.n_inputs = run.n_inputs;
+  sel.B = B;
+  if (tc->fused) {
+    // ONE cooperative launch runs every step: the chain blocks of a tile pair start step i+1
+    // as soon as the pair's selection of step i is written (counters, no host round trip)
+    const int timed = h.timing ? timing_reserve(h, 1) : 0;
+    if (timed) cudaEventRecord(h.tev[0], st);
+    static const int per_launch = getenv("FW_STEPS_PER_LAUNCH") ? atoi(getenv("FW_STEPS_PER_LAUNCH")) : 0;
+    const int chunk = per_launch > 0 ? per_launch : run.n_steps;
+    for (int i0 = 0; i0 < run.n_steps; i0 += chunk) {
+      ca.n_steps = std::min(chunk, run.n_steps - i0);
+      ca.t0 = run.t0 + i0;
+      for (int l = 0; l < L; ++l) ca.slot0[l] = (int32_t)(ca.t0 % h.dil[l]);
+      ca.sel = sel;
+      ca.sel.out_base = run.out + (size_t)i0 * B;
+      ca.sel.logits_base = run.logits ? run.logits + (size_t)i0 * B * d.A : nullptr;
+      ca.sel.n_logit_steps = run.n_logit_steps - i0;
+      ca.sel.inputs = run.inputs + (size_t)std::min(i0, run.n_inputs) * B;
+      ca.sel.n_inputs = std::max(0, run.n_inputs - i0);
+      ca.sel.t = ca.t0;
+      ca.sel.out_cls = ca.sel.out_base;
+      ca.sel.logits = (run.logits && i0 < run.n_logit_steps) ? ca.sel.logits_base : nullptr;
+      ca.sel.next_inputs = (1 < ca.sel.n_inputs) ? ca.sel.inputs + B : nullptr;
+      e = cudaMemsetAsync(tc->zflag, 0, sizeof(uint32_t) * 4 * npairs_all, st);
+      if (e != cudaSuccess) return e;
+      e = cudaLaunchCooperativeKernel((const void*)step_kernel, dim3(grid), dim3(kChainThreads),
+                                      kargs, kChainSmem, st);
+      if (e != cudaSuccess) return e;
+    }
+    if (timed) {
+      cudaEventRecord(h.tev[1], st);
+      cudaEventRecord(h.tev[2], st);
+    }
+    h.tev_used = timed;
+    h.timed_steps = timed ? run.n_steps : 0;
+    *launches = 1;
+    return cudaGetLastError();
+  }
+  // per-step launches: the step kernel (chain only) + skip / head1 / head2 GEMMs
   const dim3 gskip(tc->ntile, S / 128), gh1(tc->ntile, H / 128), gh2(tc->ntile, 1);
   const int timed = h.timing ? timing_reserve(h, run.n_steps) : 0;
-  const int npairs = B / 128;
+  ca.n_steps = 1;
   for (int i = 0; i < run.n_steps; ++i) {
-    for (int l = 0; l < L; ++l)
-      ca.qbase[l] = qoff[l] + ((run.t0 + i) % h.dil[l]) * (int64_t)(B / kChainRows) * kSlotBytes;
+    ca.t0 = run.t0 + i;
+    for (int l = 0; l < L; ++l) ca.slot0[l] = (int32_t)((run.t0 + i) % h.dil[l]);
     sel.t = run.t0 + i;
     sel.logits = (run.logits && i < run.n_logit_steps) ? run.logits + (size_t)i * B * d.A : nullptr;
     sel.out_cls = run.out + (size_t)i * B;
     sel.next_inputs = (i + 1 < run.n_inputs) ? run.inputs + (size_t)(i + 1) * B : nullptr;
     h2.sel = sel;
-    ca.sel = sel;
-    if (tc->fused) {  // zflag | sflag | hflag of every tile pair restart at 0 each step
-      cudaError_t me = cudaMemsetAsync(tc->zflag, 0, sizeof(uint32_t) * 3 * npairs, st);
-      if (me != cudaSuccess) return me;
-    }
+    static const bool dbg = getenv("FW_DEBUG_SYNC") != nullptr;
+    auto chk = [&](const char* what) {
+      if (!dbg) return;
+      cudaError_t ce = cudaStreamSynchronize(st);
+      if (ce != cudaSuccess) fprintf(stderr, "fw debug: %s failed: %s\n", what, cudaGetErrorString(ce));
+    };
     if (i < timed) cudaEventRecord(h.tev[3 * i], st);
-    if (tc->fused) {
-      cudaError_t le = cudaLaunchCooperativeKernel((const void*)step_kernel, dim3(grid),
-                                                   dim3(kChainThreads), kargs, kChainSmem, st);
-      if (le != cudaSuccess) return le;
-    } else {
-      step_kernel<<<grid, kChainThreads, kChainSmem, st>>>(ca);
-    }
+    step_kernel<<<grid, kChainThreads, kChainSmem, st>>>(ca);
+    chk("step_kernel");
     if (i < timed) cudaEventRecord(h.tev[3 * i + 1], st);
-    if (!tc->fused) gemm_kernel<128, 0><<<gskip, kGemmThreads, gemm_smem<128>(), st>>>(skip);
-    if (!tc->heads) {
-      gemm_kernel<128, 0><<<gh1, kGemmThreads, gemm_smem<128>(), st>>>(h1);
-      gemm_kernel<256, 1><<<gh2, kGemmThreads, gemm_smem<256>(), st>>>(h2);
-    }
+    gemm_kernel<128, 0><<<gskip, kGemmThreads, gemm_smem<128>(), st>>>(skip);
+    chk("skip gemm");
+    gemm_kernel<128, 0><<<gh1, kGemmThreads, gemm_smem<128>(), st>>>(h1);
+    chk("head1 gemm");
+    gemm_kernel<256, 1><<<gh2, kGemmThreads, gemm_smem<256>(), st>>>(h2);
+    chk("head2 gemm");
     if (i < timed) cudaEventRecord(h.tev[3 * i + 2], st);
   }
   h.tev_used = timed;
-  *launches = (tc->heads ? 1 : tc->fused ? 3 : 4) * (int64_t)run.n_steps;
+  h.timed_steps = timed;
+  *launches = 4 * (int64_t)run.n_steps;
+  if (getenv("FW_DEBUG_SYNC")) {
+    cudaError_t ce = cudaStreamSynchronize(st);
+    fprintf(stderr, "fw debug: unfused %d steps done: %s\n", run.n_steps, cudaGetErrorString(ce));
+  }
   return cudaGetLastError();
 }
 

@@ -50,7 +50,7 @@
 // x_full -> next layer's x_{t-d} N-half 1.
 
 constexpr int kChainRows = 64;
-constexpr int kChainThreads = 448;
+constexpr int kChainThreads = 480;  // 15 warps; 128 registers per thread (4 warps per SMSP)
 constexpr int kQueueWarp0 = 10;
 constexpr uint32_t kP1 = 16u << 16;  // lane offset of plane P1
 constexpr uint32_t kColXt = 256, kColXd = 320;  // P0
@@ -66,7 +66,11 @@ constexpr uint32_t kSkipStage = 2 * kTile + 65536;
 constexpr uint32_t kSkipBars = 2 * kSkipStage;
 constexpr uint32_t kTailStage = 2 * (kTile + 32768);  // 2 K-chunks of A | 2 of B (N <= 256)
 constexpr int kTailStages = 2;
-constexpr size_t kChainSmem = 1024 + (kOffBars > kSkipBars ? kOffBars : kSkipBars) + 256 + 4096 + 4096;
+// chain role: after its barriers, two 16 KB staging buffers for popped ring slots
+constexpr uint32_t kOffXq = kOffBars + 1024;
+constexpr size_t kChainSmem = 1024 + (kOffXq + 2 * kSlotBytes > kSkipBars + 8448
+                                          ? kOffXq + 2 * kSlotBytes
+                                          : kSkipBars + 8448);
 
 // z stash row base of (tile, layer): [tile pair][L][16 pieces][128 rows][16 B]
 __device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int L, int l) {
@@ -119,18 +123,18 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
   // fused heads' operand stream: 2 K-chunks per stage; A (the s / h images) by warp 0, B (the
   // W1 / W2 chunks) by warp 11 -- the copy engine's cost is per operation and a thread's
   // copies run one after another (tools/ring_bw.cu)
-  auto tail_loads = [&](bool is_b) {
+  const int it1 = k1 / 2, it2 = sel_block ? k2 / 2 : 0, nit = it1 + it2;
+  auto tail_loads = [&](bool is_b, int step) {
     const uint32_t b1 = (uint32_t)n1 * 128, b2 = (uint32_t)a.sel.A * 128;
-    const int it1 = k1 / 2, it2 = sel_block ? k2 / 2 : 0;
-    for (int it = 0; it < it1 + it2; ++it) {
-      const int st = it % kTailStages;
-      mbar_wait(tempty + st, ((uint32_t)(it / kTailStages) & 1) ^ 1);
+    for (int it = 0; it < nit; ++it) {
+      const int T = step * nit + it, st = T % kTailStages;
+      mbar_wait(tempty + st, ((uint32_t)(T / kTailStages) & 1) ^ 1);
       if (it == 0) {
-        wait_counter(a.sflag + p, (uint32_t)nsk);
+        wait_counter(a.sflag + p, (uint32_t)(nsk * (step + 1)));
         fence_proxy_async_all();
       }
       if (it == it1) {
-        wait_counter(a.hflag + p, (uint32_t)nsk);
+        wait_counter(a.hflag + p, (uint32_t)(nsk * (step + 1)));
         fence_proxy_async_all();
       }
       const bool two = it >= it1;
@@ -151,26 +155,29 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
   };
   if (warp == 0) {
     if (lane == 0) {  // producer: z tile of (p, l) once both chain tiles stashed it
-      for (int l = 0; l < L; ++l) {
-        const int st = l & 1;
-        mbar_wait(empty + st, ((uint32_t)(l >> 1) & 1) ^ 1);
-        wait_counter(a.zflag + p, 2u * (uint32_t)(l + 1));
-        if (l == L - 1) trace_g(a, k == 0, 2);
-        fence_proxy_async_all();
-        uint8_t* stage = smem + st * kSkipStage;
-        mbar_arrive_expect_tx(full + st, 2 * kTile + bbytes);
-        bulk_g2s(stage, a.zimg + ((size_t)p * L + l) * 2 * kTile, 2 * kTile, full + st);
-        bulk_g2s(stage + 2 * kTile, a.wskip2 + ((size_t)e * L + l) * bbytes, bbytes, full + st);
+      for (int i = 0; i < a.n_steps; ++i) {
+        for (int l = 0; l < L; ++l) {
+          const int g = i * L + l, st = g & 1;
+          mbar_wait(empty + st, ((uint32_t)(g >> 1) & 1) ^ 1);
+          wait_counter(a.zflag + p, 2u * (uint32_t)(g + 1));
+          if (l == L - 1) trace_g(a, k == 0, 2);
+          fence_proxy_async_all();
+          uint8_t* stage = smem + st * kSkipStage;
+          mbar_arrive_expect_tx(full + st, 2 * kTile + bbytes);
+          bulk_g2s(stage, a.zimg + ((size_t)p * L + l) * 2 * kTile, 2 * kTile, full + st);
+          bulk_g2s(stage + 2 * kTile, a.wskip2 + ((size_t)e * L + l) * bbytes, bbytes, full + st);
+        }
+        if (heads) tail_loads(false, i);
       }
-      if (heads) tail_loads(false);
     }
   } else if (warp == 1) {
     const uint32_t s0 = smem_u32(smem);
-    {
+    const int ntacc = sel_block ? 2 : 1;
+    for (int i = 0; i < a.n_steps; ++i) {
       const uint32_t id = idesc_f16(128, SK);
       for (int l = 0; l < L; ++l) {
-        const int st = l & 1;
-        mbar_wait(full + st, (uint32_t)(l >> 1) & 1);
+        const int gl = i * L + l, st = gl & 1;
+        mbar_wait(full + st, (uint32_t)(gl >> 1) & 1);
         tc_fence_after();
         const uint32_t sa = s0 + st * kSkipStage, sb = sa + 2 * kTile;
         if (elect_one()) {
@@ -187,19 +194,18 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
       if (elect_one()) mma_commit(acc_full);
       __syncwarp();
       trace_g(a, k == 0 && lane == 0, 7);
-    }
-    if (heads) {
-      const int it1 = k1 / 2;
-      for (int g = 0; g < (sel_block ? 2 : 1); ++g) {
+      if (!heads) continue;
+      for (int g = 0; g < ntacc; ++g) {
         const int nb = g == 0 ? n1 : a.sel.A;
-        const uint32_t id = idesc_f16(128, nb);
-        mbar_wait(tfree, (uint32_t)g);  // the epilogue has read the previous accumulator
+        const uint32_t idh = idesc_f16(128, nb);
+        // the epilogue has read the previous accumulator (2 tfree phases per step)
+        mbar_wait(tfree, (uint32_t)(2 * i + g) & 1);
         tc_fence_after();
         trace_g(a, k == 0 && lane == 0, 8 + 3 * g);
         const int i0 = g == 0 ? 0 : it1, ni = g == 0 ? it1 : k2 / 2;
         for (int it = i0; it < i0 + ni; ++it) {
-          const int st = it % kTailStages;
-          mbar_wait(tfull + st, (uint32_t)(it / kTailStages) & 1);
+          const int T = i * nit + it, st = T % kTailStages;
+          mbar_wait(tfull + st, (uint32_t)(T / kTailStages) & 1);
           tc_fence_after();
           const uint32_t sa = s0 + st * kTailStage, sb = sa + 2 * kTile;
           if (it == i0) trace_g(a, k == 0 && lane == 0, 9 + 3 * g);
@@ -209,7 +215,7 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk)
                 mma_bf16(tmem, sdesc_sw128(sa + c * kTile + kk * 32),
-                         sdesc_sw128(sb + c * (uint32_t)nb * 128 + kk * 32), id,
+                         sdesc_sw128(sb + c * (uint32_t)nb * 128 + kk * 32), idh,
                          (it > i0 || c || kk) ? 1u : 0u);
             mma_commit(tempty + st);
           }
@@ -228,29 +234,30 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
     for (int i = threadIdx.x - 64; i < SK + (heads ? n1 : 0); i += 256)
       sbias[i] = i < SK ? a.skip_bsum[e * SK + i] : a.h1_b[e * n1 + (i - SK)];
     named_bar_sync(1, 256);
-    mbar_wait(acc_full, 0);
-    tc_fence_after();
-    trace_g(a, k == 0 && warp == 2 && lane == 0, 14);
-    // ReLU(s + bias) -> this block's SK/64 chunks of the pair's s images: staged in shared
-    // memory (the tail ring is idle now) and written with one bulk store -- per-thread
-    // 16-byte stores of swizzled rows would touch 32 lines per warp instruction
     const uint32_t stg = smem_u32(smem);
-    epi_relu_image_smem(trow, r, h * (SK / 2), SK / 2, h * (SK / 2), sbias, stg + h * (SK / 128) * kTile);
-    fence_proxy_async();
-    tc_fence_before();
-    if (heads) mbar_arrive(tfree);  // s read out of TMEM
-    named_bar_sync(1, 256);
-    if (warp == 2 && lane == 0) {
-      bulk_s2g(a.simg + ((size_t)p * (S / 64) + e * SK / 64) * kTile, smem, (uint32_t)SK * 256);
-      bulk_commit();
-      bulk_wait0();
-      fence_proxy_async_all();
-      if (heads) red_release_gpu(a.sflag + p, 1u);
-      trace_g(a, k == 0, 3);
-    }
-    if (heads) {
+    for (int i = 0; i < a.n_steps; ++i) {
+      mbar_wait(acc_full, (uint32_t)i & 1);
+      tc_fence_after();
+      trace_g(a, k == 0 && warp == 2 && lane == 0, 14);
+      // ReLU(s + bias) -> this block's SK/64 chunks of the pair's s images: staged in shared
+      // memory (the rings are idle now) and written with one bulk store -- per-thread
+      // 16-byte stores of swizzled rows would touch 32 lines per warp instruction
+      epi_relu_image_smem(trow, r, h * (SK / 2), SK / 2, h * (SK / 2), sbias, stg + h * (SK / 128) * kTile);
+      fence_proxy_async();
+      tc_fence_before();
+      if (heads) mbar_arrive(tfree);  // s read out of TMEM
+      named_bar_sync(1, 256);
+      if (warp == 2 && lane == 0) {
+        bulk_s2g(a.simg + ((size_t)p * (S / 64) + e * SK / 64) * kTile, smem, (uint32_t)SK * 256);
+        bulk_commit();
+        bulk_wait0();
+        fence_proxy_async_all();
+        if (heads) red_release_gpu(a.sflag + p, 1u);
+        trace_g(a, k == 0, 3);
+      }
+      if (!heads) continue;
       // head1 part: h columns [e*n1, (e+1)*n1) -> the pair's h images
-      mbar_wait(tacc, 0);
+      mbar_wait(tacc, (uint32_t)(i * (sel_block ? 2 : 1)) & 1);
       tc_fence_after();
       trace_g(a, k == 0 && warp == 2 && lane == 0, 15);
       // the tail ring holds no live operands once head1's accumulator is complete
@@ -270,34 +277,48 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
         trace_g(a, k == 0, 4);
       }
       if (sel_block) {  // head2 logits + the selection rule for the pair's 128 streams
-        mbar_wait(tacc, 1);
-        if (a.sel.mode == FW_SAMPLE_GUMBEL) mbar_wait(noise_ready, 0);
+        mbar_wait(tacc, (uint32_t)(2 * i + 1) & 1);
+        if (a.sel.mode == FW_SAMPLE_GUMBEL) mbar_wait(noise_ready, (uint32_t)i & 1);
         tc_fence_after();
         trace_g(a, k == 0 && warp == 2 && lane == 0, 5);
-        epi_select(trow, r, h, p * 128 + r, a.sel, xch, 256);
-        trace_g(a, k == 0 && warp == 2 && lane == 0, 6);
+        const SelectArgs sel = sel_step(a.sel, a.t0, i);
+        epi_select(trow, r, h, p * 128 + r, sel, xch, 256);
+        // every selection of the pair is written: the chain blocks may start step i+1
+        tc_fence_before();
+        named_bar_sync(1, 256);
+        if (warp == 2 && lane == 0) {
+          red_release_gpu(a.cls_ready + p, 1u);
+          trace_g(a, k == 0, 6);
+        }
       }
     }
   } else if (warp >= 10 && warp < 14) {
-    if (sel_block && a.sel.mode == FW_SAMPLE_GUMBEL) {
-      // the step's Gumbel noise of row r (stream p*128 + r), 256 classes -> TMEM [256,512)
-      const int sub = warp & 3;
-      const int r = sub * 32 + lane;
-      const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
-      const uint32_t prefix = noise_prefix(a.sel.seed, (uint32_t)(a.sel.stream_offset + p * 128 + r),
-                                           (uint32_t)a.sel.t);
+    // per step: the Gumbel noise (selecting block), then warp 11's half of the head operands
+    const bool noise = sel_block && a.sel.mode == FW_SAMPLE_GUMBEL;
+    const int sub = warp & 3;
+    const int r = sub * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
+    for (int i = 0; i < a.n_steps; ++i) {
+      if (noise) {
+        // step i's noise of row r (stream p*128 + r), 256 classes -> TMEM [256,512), once
+        // the previous step's selection has read the previous noise
+        const uint32_t prefix = noise_prefix(a.sel.seed, (uint32_t)(a.sel.stream_offset + p * 128 + r),
+                                             (uint32_t)(a.t0 + i));
+        if (i > 0) wait_counter(a.cls_ready + p, (uint32_t)i);
 #pragma unroll 1
-      for (int cc = 0; cc < 8; ++cc) {
-        float gn[32];
+        for (int cc = 0; cc < 8; ++cc) {
+          float gn[32];
 #pragma unroll
-        for (int i = 0; i < 32; ++i) gn[i] = gumbel_noise(prefix, 32 * cc + i);
-        tmem_st32(trow + 256 + 32 * cc, gn);
+          for (int j = 0; j < 32; ++j) gn[j] = gumbel_noise(prefix, 32 * cc + j);
+          tmem_st32(trow + 256 + 32 * cc, gn);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(noise_ready);
       }
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(noise_ready);
+      if (warp == 11 && lane == 0 && heads) tail_loads(true, i);
+      __syncwarp();
     }
-    if (warp == 11 && lane == 0 && heads) tail_loads(true);
   }
   tc_fence_before();
   __syncthreads();
@@ -339,10 +360,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
   uint64_t* z1_ready = bars + 16;  // 256
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
   uint64_t* xd_free = bars + 18;   // commit: this layer's x_{t-d} MMAs are done with TMEM xd
+  uint64_t* z_stashed = bars + 21;  // 128: queue warps' z stash stores of this layer issued
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
   const int L = a.L;
+  const int G = a.n_steps * L;  // layers of all steps of this launch, in order
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 11; ++i) mbar_init(bars + i, 1);
@@ -353,6 +376,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     mbar_init(z0_ready, 256);
     mbar_init(z1_ready, 256);
     mbar_init(xd_free, 1);
+    mbar_init(z_stashed, 128);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -363,9 +387,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
 
   if (warp == 0) {
     if (lane == 0) {  // ---- weight producer ----
-      for (int l = 0; l < L; ++l) {
+      int gc = 0;  // res stages loaded (all but each step's top layer)
+      for (int g = 0; g < G; ++g) {
+        const int l = g % L;
         const uint8_t* wl = a.w + (size_t)l * kLayerBytes;  // A0 | A1 | B | C
-        const uint32_t ph = ((uint32_t)l & 1) ^ 1;
+        const uint32_t ph = ((uint32_t)g & 1) ^ 1;
         mbar_wait(emptyA0, ph);
         trace_at(a, l, T_PROD_A0, clock64());
         mbar_arrive_expect_tx(fullA0, kStageA);
@@ -379,10 +405,11 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         mbar_arrive_expect_tx(fullB, kStageB);
         bulk_g2s(stB, wl + 2 * kStageA, kStageB, fullB);
         if (l + 1 < L) {
-          mbar_wait(emptyC, ph);
+          mbar_wait(emptyC, ((uint32_t)gc & 1) ^ 1);
           trace_at(a, l, T_PROD_C, clock64());
           mbar_arrive_expect_tx(fullC, kStageC);
           bulk_g2s(stC, wl + 2 * kStageA + kStageB, kStageC, fullC);
+          ++gc;
         }
       }
     }
@@ -414,16 +441,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
                       id, (c | kk) ? 1u : 0u);
       mma_commit(hh ? emptyA1 : emptyA0);
     };
-    // warp-uniform non-blocking probe: layer lx's x_{t-d} operand and weight stage
-    auto ready = [&](int lx, uint64_t* stage) {
-      const uint32_t pn = (uint32_t)lx & 1;
-      int ok = lane == 0 ? (mbar_test(xd_ready, pn) && mbar_test(stage, pn)) : 0;
-      return __shfl_sync(0xffffffffu, ok, 0) != 0;
-    };
     bool early[2] = {false, false};
-    for (int l = 0; l < L; ++l) {
-      const uint32_t par = (uint32_t)l & 1;
-      const bool nx = l + 1 < L;
+    int gc = 0;  // res layers issued (parity of fullC)
+    for (int g = 0; g < G; ++g) {
+      const int l = g % L;
+      const uint32_t par = (uint32_t)g & 1;
+      const bool nx = l + 1 < L, nxg = g + 1 < G;
       if (lane == 0) trace_at(a, l, T_H0_EARLY, (early[0] ? 1 : 0) + (early[1] ? 2 : 0));
       if (!early[0] || !early[1]) {
         mbar_wait(xd_ready, par);
@@ -445,8 +468,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         mma_tmem_a(tmem + 0, tmem + kColXt + 32, sb + 1 * kChunk);
       }
       __syncwarp();
-      // the gate warps rewrite z after acc0_full: layer l-1's stash has read it
-      if (l > 0) mbar_wait(z_read, par ^ 1);
+      // the gate warps rewrite z after acc0_full: the previous layer's stash has read it
+      if (g > 0) mbar_wait(z_read, par ^ 1);
       if (elect_one()) mma_commit(acc0_full);
       __syncwarp();
       if (lane == 0) trace_at(a, l, T_MMA_ACC0, clock64());
@@ -472,16 +495,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       if (lane == 0) trace_at(a, l, T_MMA_Z0, clock64());
       tc_fence_after();
       if (nx) {
-        wait_w(fullC, par);
+        wait_w(fullC, (uint32_t)gc & 1);
         if (elect_one()) mma_tmem_a(tmem + kP1 + kColX, tmem + kP1 + kColZ + 0, sc + 0 * kChunk);
         __syncwarp();
-        // acc0 is free (gate half 0 done): layer l+1's x_{t-d} N-half 0. Its operand follows
-        // this layer's x_{t-d} MMAs (xd_free) within a few hundred cycles and its weights
-        // loaded a layer ago, so waiting here costs little; issued after x_full instead it
-        // would sit in front of the next layer's x_t MMAs.
-        mbar_wait(xd_ready, (uint32_t)(l + 1) & 1);
+      }
+      if (nxg) {
+        // acc0 is free (gate half 0 done): the next layer's x_{t-d} N-half 0 (the next
+        // step's layer 0 included -- it needs no input class). Its operand follows this
+        // layer's x_{t-d} MMAs (xd_free) within a few hundred cycles and its weights loaded a
+        // layer ago, so waiting here costs little; issued after x_full instead it would sit
+        // in front of the next layer's x_t MMAs.
+        mbar_wait(xd_ready, par ^ 1);
         tc_fence_after();
-        wait_w(fullA0, (uint32_t)(l + 1) & 1);
+        wait_w(fullA0, par ^ 1);
         if (elect_one()) xd_half(0);
         __syncwarp();
         early[0] = true;
@@ -499,14 +525,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         mbar_wait(x_pushed, par);
         if (elect_one()) mma_commit(x_full);
         __syncwarp();
+        ++gc;
         if (lane == 0) trace_at(a, l, T_MMA_XFULL, clock64());
-        // acc1 is free (gate half 1 done): layer l+1's x_{t-d} halves still pending
-        if (!early[0] && ready(l + 1, fullA0)) {
-          tc_fence_after();
-          if (elect_one()) xd_half(0);
-          __syncwarp();
-          early[0] = true;
-        }
         // (x_{t-d} half 1 stays in the layer: issued here it would hold the tensor pipe
         // and this warp when the next layer's x_t MMAs become ready)
       }
@@ -522,29 +542,46 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     const bool pf = warp == kQueueWarp0 && lane == 0;
     const bool tq = pf;
     const uint8_t* qtile = a.queue + (size_t)tile * kSlotBytes;
-    if (pf)
-      for (int l = 0; l < 2 && l < L; ++l) bulk_prefetch_l2(qtile + a.qbase[l], kSlotBytes);
-    // K-piece j (K 8j..8j+7) of row r is the 16 bytes at (j * 64 + r) * 16: packed words
-    // 4j .. 4j+3 of the operand row
-    uint32_t xd[64];
-    auto load_slot = [&](int l) {
-      const uint4* src = reinterpret_cast<const uint4*>(qtile + a.qbase[l]) + r;
+    auto qb = [&](int g) { return qbase_of(a, g / L, g % L); };
+    // pops: each thread copies its own row of layer g's slot into staging buffer Xq[g & 1]
+    // (16 x 16 B, cp.async) two layers ahead -- no registers held across layers, and the
+    // same thread wrote that row with its push, so plain program order covers the reuse of
+    // ring slots within a launch. K-piece j (K 8j..8j+7) of row r is the 16 bytes at
+    // (j * 64 + r) * 16: packed words 4j .. 4j+3 of the operand row.
+    uint8_t* xq = smem + kOffXq;
+    auto load_slot = [&](int g) {
+      if (act) {
+        const uint8_t* src = qtile + qb(g) + (size_t)r * 16;
+        const uint32_t dst = smem_u32(xq + (g & 1) * kSlotBytes) + (uint32_t)r * 16;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) cp_async16(dst + (uint32_t)j * kChainRows * 16, src + (size_t)j * kChainRows * 16);
+      }
+      cp_async_commit();
+    };
+    // row r of layer g's x_{t-d} -> TMEM xd (lanes 16..31 store zeros into P1's scratch
+    // columns), then the copy of layer g+2 into the freed buffer
+    auto store_xd = [&](int g) {
+      cp_async_wait<1>();  // layer g's copies done (g+1's may be in flight)
+      const uint32_t src = smem_u32(xq + (g & 1) * kSlotBytes) + (uint32_t)r * 16;
+      uint32_t xd[64];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const uint4 v = act ? src[j * kChainRows] : make_uint4(0, 0, 0, 0);
-        xd[4 * j] = v.x;
-        xd[4 * j + 1] = v.y;
-        xd[4 * j + 2] = v.z;
-        xd[4 * j + 3] = v.w;
+        uint32_t v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+        if (act)
+          asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                       : "=r"(v0), "=r"(v1), "=r"(v2), "=r"(v3)
+                       : "r"(src + (uint32_t)j * kChainRows * 16));
+        xd[4 * j] = v0;
+        xd[4 * j + 1] = v1;
+        xd[4 * j + 2] = v2;
+        xd[4 * j + 3] = v3;
       }
-    };
-    // (lanes 16..31 store zeros into P1's scratch columns under xd)
-    auto store_xd = [&]() {
       tmem_st32(trow + kColXd, *reinterpret_cast<float(*)[32]>(xd));
       tmem_st32(trow + kColXd + 32, *reinterpret_cast<float(*)[32]>(xd + 32));
-      tmem_wait_st();
       tc_fence_before();
       mbar_arrive(xd_ready);
+      if (g + 2 < G) load_slot(g + 2);
+      else cp_async_commit();  // keep one group per layer for the wait count
     };
     // 64 TMEM columns of packed fp16 pairs (32x32b: lanes 0..15 read P0, 16..31 read P1)
     // -> 16 K-pieces at dst (+ j * stride rows) from the lanes with `mine`
@@ -564,27 +601,28 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       }
     };
     load_slot(0);
-    store_xd();
-    if (L > 1) load_slot(1);
-    for (int l = 0; l < L; ++l) {
-      const uint32_t par = (uint32_t)l & 1;
-      if (pf && l + 2 < L) bulk_prefetch_l2(qtile + a.qbase[l + 2], kSlotBytes);
-      // push x_l (P0 xt columns, lanes 0..15) into ring slot (t mod d_l); this thread's own
-      // loads of that slot completed before store_xd of this layer
+    if (G > 1) load_slot(1);
+    else cp_async_commit();
+    store_xd(0);
+    for (int g = 0; g < G; ++g) {
+      const int l = g % L;
+      const uint32_t par = (uint32_t)g & 1;
+      // push x_l (P0 xt columns, lanes 0..15) into ring slot (t mod d_l); this thread's pop
+      // of its row of that slot completed before store_xd of this layer
       mbar_wait(xt_ready, par);
       tc_fence_after();
-      tmem_to_pieces(kColXt, reinterpret_cast<uint4*>(const_cast<uint8_t*>(qtile) + a.qbase[l]) + r,
+      tmem_to_pieces(kColXt, reinterpret_cast<uint4*>(const_cast<uint8_t*>(qtile) + qb(g)) + r,
                      kChainRows, act);
       tc_fence_before();
       mbar_arrive(x_pushed);
       if (tq) trace_at(a, l, T_Q_LOAD, clock64());
-      // x_{t-d} of layer l+1 -> TMEM xd once layer l's x_{t-d} MMAs are done (xd_free)
-      if (l + 1 < L) {
+      // x_{t-d} of the next layer -> TMEM xd once this layer's x_{t-d} MMAs are done
+      if (g + 1 < G) {
         mbar_wait(xd_free, par);
+        if (tq) trace_at(a, (g + 1) % L, T_G0_STS, clock64());
         tc_fence_after();
-        store_xd();
-        if (tq) trace_at(a, l + 1, T_Q_XD, clock64());
-        if (l + 2 < L) load_slot(l + 2);  // in flight during layer l+1
+        store_xd(g + 1);
+        if (tq) trace_at(a, (g + 1) % L, T_Q_XD, clock64());
       }
       // z stash of layer l (P1 z columns: lanes 16..31 of the quadrant hold the rows)
       mbar_wait(z1_ready, par);
@@ -592,11 +630,18 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       tmem_to_pieces(kColZ, zstash_rows(a.zimg, tile, L, l) + r, 2 * kChainRows, !act);
       tc_fence_before();
       mbar_arrive(z_read);
-      if (a.zflag != nullptr) {  // publish z_l of this tile to the skip blocks
-        named_bar_sync(1, 128);
-        if (warp == kQueueWarp0 && lane == 0) red_release_gpu(a.zflag + (tile >> 1), 1u);
-      }
+      mbar_arrive(z_stashed);  // warp 14 publishes them (its release fence waits on the stores)
+      if (tq) trace_at(a, l, T_SP2, clock64());
       if (tq) trace_at(a, l, T_SP1, clock64());
+      if (tq) trace_at(a, l, T_SP3, clock64());
+    }
+  } else if (warp == 14) {
+    // ---- publisher: z_l of this tile -> the tail blocks (release of the stash stores) ----
+    if (lane == 0 && a.zflag != nullptr) {
+      for (int g = 0; g < G; ++g) {
+        mbar_wait(z_stashed, (uint32_t)g & 1);
+        red_release_gpu(a.zflag + (tile >> 1), 1u);
+      }
     }
   } else if (warp >= 2 && warp < 10) {
     // ---- gate warps: quadrant q, half h; 16x64b accesses: lane t holds row
@@ -605,7 +650,6 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const int pc = (lane >> 1) & 1;
     const int row = q * 16 + (lane >> 2) + 8 * (lane & 1);
-    const int c = a.cls[tile * kChainRows + row];
     const bool tr = (warp == 2 && lane == 0);
     // pack own fp16 pairs (v[2i], v[2i+1]) -- columns 4i+pc, 4i+2+pc -- and complete the
     // operand pairs with the partner lane (t ^ 2): parity 0 keeps the low halves (packed
@@ -614,20 +658,26 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       const uint32_t o = __shfl_xor_sync(0xffffffffu, w, 2);
       return pc == 0 ? __byte_perm(w, o, 0x5410) : __byte_perm(o, w, 0x7632);
     };
-    trace_g(a, tr, 0);
-    for (int l = 0; l < L; ++l) {
-      const uint32_t par = (uint32_t)l & 1;
+    int gx = 0;  // x_full phases seen
+    for (int g = 0; g < G; ++g) {
+      const int i = g / L, l = g % L;
+      const uint32_t par = (uint32_t)g & 1;
+      if (l == 0) trace_g(a, tr, 0);
       if (tr) trace_at(a, l, T_EPI_A, clock64());
       // x_l channels 64h + 2j + pc (j < 32): the embedding at l = 0, else the P1 residual
       // stream (+ the pending bias)
       uint32_t xv[32];
       if (l == 0) {
+        // step i's input class: written by the pair's selection of step i-1
+        if (i > 0) wait_counter(a.cls_ready + (tile >> 1), (uint32_t)i);
+        const int c = a.cls[tile * kChainRows + row];
         const float* e = a.embed + (size_t)c * kR + 64 * h + pc;
 #pragma unroll
         for (int j = 0; j < 32; ++j) xv[j] = __float_as_uint(__ldg(e + 2 * j));
         tmem_st_16x64b_x32(trow + kP1 + kColX + 64 * h, xv);
       } else {
-        mbar_wait(x_full, par ^ 1);
+        mbar_wait(x_full, (uint32_t)gx & 1);
+        ++gx;
         if (tr) trace_at(a, l, T_EPI_XFULL, clock64());
         tc_fence_after();
         tmem_ld_16x64b_x32(trow + kP1 + kColX + 64 * h, xv);
@@ -693,8 +743,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         mbar_arrive(hh == 0 ? z0_ready : z1_ready);
         if (tr) trace_at(a, l, hh == 0 ? T_EPI_Z0 : T_EPI_Z1, clock64());
       }
+      if (l == L - 1) trace_g(a, tr, 1);
     }
-    trace_g(a, tr, 1);
   }
   tc_fence_before();
   __syncthreads();

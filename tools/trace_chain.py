@@ -23,7 +23,7 @@ from paper_1611_09482_b200 import CellGenerator, Sampler, _lib, build_cell_model
 NAMES = ["mma_xd", "mma_xt", "mma_acc0", "mma_acc1", "mma_z0", "mma_z1", "mma_xful", "mma_wwai",
          "epi_a", "epi_xful", "epi_xt", "epi_acc0", "epi_z0", "epi_acc1", "epi_z1", "h0_early",
          "q_xd", "q_load", "prod_a0", "prod_a1", "prod_b", "prod_c", "g0_ld", "g0_math",
-         "g0_sts", "pushed", "g1_ld", "g1_math", "g1_sts", "q_stash", "sp2", "sp3"]
+         "q_xdfree", "q_xqfull", "g1_ld", "g1_math", "q_bar", "q_rel", "q_stash", "q_end"]
 RAW = {7, 15}  # counts / flags, not timestamps
 SLOTS = len(NAMES)
 
