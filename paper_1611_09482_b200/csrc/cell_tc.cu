@@ -236,9 +236,7 @@ __device__ __forceinline__ void epi_relu_image(uint32_t trow, int r, int c0, int
                                                const float* bias, uint8_t* img) {
   for (int cc = 0; cc < ncols / 64; ++cc) {
     float v[64];
-    tmem_ld32(trow + c0 + 64 * cc, *reinterpret_cast<float(*)[32]>(v));
-    tmem_ld32(trow + c0 + 64 * cc + 32, *reinterpret_cast<float(*)[32]>(v + 32));
-    tmem_wait_ld();
+    tmem_ld64(trow + c0 + 64 * cc, v);
     const int n = n0 + 64 * cc;
 #pragma unroll
     for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + bias[n + i], 0.f);
@@ -257,9 +255,7 @@ __device__ __forceinline__ void epi_relu_image_smem(uint32_t trow, int r, int c0
                                                     int n0, const float* bias, uint32_t sdst) {
   for (int cc = 0; cc < ncols / 64; ++cc) {
     float v[64];
-    tmem_ld32(trow + c0 + 64 * cc, *reinterpret_cast<float(*)[32]>(v));
-    tmem_ld32(trow + c0 + 64 * cc + 32, *reinterpret_cast<float(*)[32]>(v + 32));
-    tmem_wait_ld();
+    tmem_ld64(trow + c0 + 64 * cc, v);
     const int n = n0 + 64 * cc;
 #pragma unroll
     for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + bias[n + i], 0.f);

@@ -708,16 +708,14 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         mbar_wait(hh == 0 ? acc0_full : acc1_full, par);
         if (tr) trace_at(a, l, hh == 0 ? T_EPI_ACC0 : T_EPI_ACC1, clock64());
         tc_fence_after();
-        uint32_t ta[16], sa[16];
-        tmem_ld_16x64b_x16(trow + 128 * hh + 32 * h, ta);
-        tmem_ld_16x64b_x16(trow + 128 * hh + 64 + 32 * h, sa);
-        tmem_wait_ld();
+        uint32_t ts[32];  // tanh columns | sigmoid columns
+        tmem_ld_16x64b_x16_2(trow + 128 * hh + 32 * h, trow + 128 * hh + 64 + 32 * h, ts);
         if (tr) trace_at(a, l, hh == 0 ? T_G0_LD : T_G1_LD, clock64());
         float at[16], as[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          at[j] = __uint_as_float(ta[j]);
-          as[j] = __uint_as_float(sa[j]);
+          at[j] = __uint_as_float(ts[j]);
+          as[j] = __uint_as_float(ts[16 + j]);
         }
         if (a.has_dil_bias) {
           const int j0 = 64 * hh + 32 * h + pc;
