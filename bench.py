@@ -110,35 +110,30 @@ class ClockSampler:
 
 
 # ---- workload accounting --------------------------------------------------------------
-def step_accounting(cell, batch):
-    """Algorithmic FLOPs and bytes of one step."""
+def step_accounting(cell, batch, queue_elem_bytes=4):
+    """Algorithmic FLOPs and bytes of one step: every layer's
+    dilated + residual + skip projections and the two head layers for every stream, the
+    weights once, one ring slot read + one written per layer per stream (fp32 slots on the
+    SIMT path, fp16 operand slots on the tcgen05 path), the embedding row and class io."""
     wbytes = 2 if cell.weight_dtype == "bf16" else 4
     flops = 2 * cell.macs_per_sample() * batch
     weight_bytes = cell.weight_count() * wbytes
     R, N = cell.residual_channels, cell.total_layers
-    queue_bytes = batch * N * 2 * R * 4  # one slot read + one slot written per layer per stream
+    queue_bytes = batch * N * 2 * R * queue_elem_bytes
     io_bytes = batch * (R * 4 + 8)  # embedding row + class in/out
     return flops, weight_bytes + queue_bytes + io_bytes, queue_bytes
 
 
 def dominant_accounting(cell, batch, kernel):
-    """Algorithmic FLOPs and bytes per step of the dominant kernel.
-
-    tcgen05: the chain kernel -- the dilated-conv and residual projections of every layer
-    (the skip/head GEMMs run in separate launches), the chain weights once, and one queue
-    slot read + written per layer per stream. SIMT: the whole step."""
-    if kernel != "tcgen05":
-        f, b, _ = step_accounting(cell, batch)
-        return f, b
-    L, R, D = cell.total_layers, cell.residual_channels, cell.dilation_channels
-    macs = L * 4 * D * R + (L - 1) * R * D
-    wbytes = 2 * (L * (4 * D * R + R * D))
-    qbytes = batch * L * 2 * R * 4
-    return 2 * macs * batch, wbytes + qbytes + batch * R * 4
+    """Algorithmic FLOPs and bytes per step of the dominant kernel. Both paths run the whole
+    step in one kernel (tcgen05: the persistent step kernel -- chain, fused skip sum, heads
+    and selection; SIMT: the persistent cell kernel), so this is the step's accounting."""
+    f, b, _ = step_accounting(cell, batch, 2 if kernel == "tcgen05" else 4)
+    return f, b
 
 
 def traffic_per_launch(kernel):
-    """DRAM bytes of one dominant-kernel launch from the newest committed ncu summary."""
+    """DRAM bytes per step of the dominant kernel from the newest committed ncu summary."""
     want = "step_kernel" if kernel == "tcgen05" else "cell_simt_kernel"
     for f in sorted((ROOT / "profiles").glob("ncu_summary_*.json"), reverse=True):
         try:
@@ -147,7 +142,8 @@ def traffic_per_launch(kernel):
             continue
         for k in d.get("kernels", []):
             if want in k.get("kernel", "") and k.get("dram_read") is not None:
-                return k["dram_read"] + k["dram_write"], f.name
+                steps = max(int(k.get("steps_per_launch", 1)), 1)
+                return (k["dram_read"] + k["dram_write"]) / steps, f.name
     return None, None
 
 
@@ -323,8 +319,9 @@ def main():
 
     if rank == 0:
         peaks = load_peaks()
-        flops, bytes_step, qbytes = step_accounting(spec.cell, total_batch)
-        per_gpu_flops, per_gpu_bytes, _ = step_accounting(spec.cell, B)
+        qeb = 2 if gen.kernel == "tcgen05" else 4
+        flops, bytes_step, qbytes = step_accounting(spec.cell, total_batch, qeb)
+        per_gpu_flops, per_gpu_bytes, _ = step_accounting(spec.cell, B, qeb)
         s_per_step = ms / 1e3 / args.steps
         value = total_batch * args.steps / (ms / 1e3)
         tensor_peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) * 1e12
@@ -334,8 +331,8 @@ def main():
         t_flop = per_gpu_flops / comp_peak
         t_byte = per_gpu_bytes / hbm
         kname = gen.kernel
-        # dominant kernel: the tcgen05 chain kernel (one launch per step) or the SIMT
-        # kernel (one launch per generate call, all of the step's work)
+        # dominant kernel: the persistent step kernel of either path (one launch per generate
+        # call doing all of every step's work); its time per step from CUDA events
         k_flops, k_bytes = dominant_accounting(spec.cell, B, kname)
         k_s = kernel_s_per_step
         kt_flop, kt_byte = k_flops / comp_peak, k_bytes / hbm
@@ -349,7 +346,8 @@ def main():
         roof["frac"] = roof["achieved"] / roof["peak"]
         traffic, tsrc = traffic_per_launch(kname)
         roof["traffic"] = traffic
-        roof["kernel"] = ("step_kernel (chain + fused skip, one launch per step)" if kname == "tcgen05"
+        roof["kernel"] = ("step_kernel (persistent: chain + skip sum + heads + selection, one "
+                          "cooperative launch per generate call, per-step share)" if kname == "tcgen05"
                           else "cell_simt_kernel (one launch per generate call, per-step share)")
         roof["algorithmic_per_step"] = {"flop": k_flops, "bytes": k_bytes}
         roof["kernel_us_per_step"] = 1e6 * k_s
@@ -376,8 +374,9 @@ def main():
                        "layers": spec.cell.total_layers, "residual": spec.cell.residual_channels,
                        "skip": spec.cell.skip_channels, "kernel": kname,
                        "parallelism": f"streams sharded x{world}",
-                       "l2": "queues 8.6 GB >> L2; each step touches "
-                             f"{qbytes / 1e6:.0f} MB of fresh queue slots (no flush needed)"},
+                       "l2": f"queues {gen.queue_bytes / 1e9:.1f} GB >> L2 (126 MB); each step "
+                             f"touches {qbytes / 1e6:.0f} MB of fresh queue slots (no flush "
+                             "needed)"},
             "roofline": roof,
             "e2e": {"value": total_batch * args.steps / e2e_s, "unit": "samples/s",
                     "h2d_bytes_per_step": B * 4 / args.steps, "d2h_bytes_per_step": B * 4,

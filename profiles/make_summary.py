@@ -1,6 +1,7 @@
-"""Write profiles/ncu_summary_<round>.json from an ncu --set full report (+ launch list).
+"""Write profiles/ncu_summary_<tag>.json from an ncu --set full report (+ launch list).
 
-    python profiles/make_summary.py r01 gpurun_out/prof_v5.ncu-rep gpurun_out/launches_v6.csv
+    python profiles/make_summary.py r01b gpurun_out/prof_r01_step.ncu-rep \
+        gpurun_out/launches_r01_v2.csv [steps_per_launch]
 
 Per kernel: duration, DRAM bytes read/written, tensor-pipe activity, L2/L1 throughput.
 Also the per-step DRAM traffic of the cfg4 tcgen05 step (sum over its 4 kernels), which
@@ -15,6 +16,7 @@ from pathlib import Path
 
 tag, rep = sys.argv[1], sys.argv[2]
 launch_csv = sys.argv[3] if len(sys.argv) > 3 else None
+steps_per_launch = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(raw)))
@@ -32,6 +34,8 @@ scale = {"us": 1.0, "ns": 1e-3, "ms": 1e3, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1
 kernels = []
 for r in rows[2:]:
     k = {"kernel": r[ix["Kernel Name"]].split("(")[0]}
+    if "step_kernel" in k["kernel"]:
+        k["steps_per_launch"] = steps_per_launch
     for name, metric in keys.items():
         if metric in ix:
             v = r[ix[metric]].replace(",", "")
@@ -41,8 +45,17 @@ for r in rows[2:]:
                 k[name] = None
     kernels.append(k)
 out = {"round": tag, "report": Path(rep).name, "kernels": kernels}
+persist = [k for k in kernels if "step_kernel" in k["kernel"]]
+if persist:
+    k = persist[0]
+    n = k["steps_per_launch"]
+    out["cfg4_large_batch/tcgen05"] = {
+        "dram_bytes_per_step": ((k["dram_read"] or 0) + (k["dram_write"] or 0)) / n,
+        "kernels": [k["kernel"]], "steps_per_launch": n,
+        "duration_us_per_step_cold": (k["duration_us"] or 0) / n,
+        "note": "ncu --set full of one persistent launch (all steps' work); per-step = / steps"}
 step = [k for k in kernels if "chain_kernel" in k["kernel"] or "gemm_kernel" in k["kernel"]]
-if step:
+if step and not persist:
     # one chain + skip + head1 + head2 launch = one cfg4 step (the capture order)
     first = next(i for i, k in enumerate(step) if "chain_kernel" in k["kernel"])
     one = step[first:first + 4]
