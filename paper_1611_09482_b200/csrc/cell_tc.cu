@@ -161,6 +161,7 @@ struct ChainArgs {
   // fused heads (heads != 0): head1 by the pair's skip blocks (H / nsk columns each), head2
   // + selection by its first skip block; sflag / hflag count the blocks done with simg / himg
   int heads, H;
+  int pair_mode;         // tail blocks in 2-CTA clusters exchanging through DSMEM
   uint32_t* sflag;       // [B/128] (cumulative over the launch's steps)
   uint32_t* hflag;       // [B/128]
   const uint8_t* wh1b;   // [nsk][S/64][H/nsk rows][128 B]
@@ -274,26 +275,38 @@ __device__ __forceinline__ void epi_relu_image_smem(uint32_t trow, int r, int c0
 // noise_col + class (fused tail); otherwise it is hashed here.
 __device__ __forceinline__ void epi_select(uint32_t trow, int r, int h, int stream,
                                         const SelectArgs& g, float* xch, int noise_col = -1) {
-  const int HALF = g.A / 2;
+  const int HALF = g.A / 2, A = g.A, mode = g.mode;
+  const float* __restrict__ bias = g.bias;
   const uint32_t prefix = noise_prefix(g.seed, (uint32_t)(g.stream_offset + stream), (uint32_t)g.t);
   const int cbase = h * HALF;
-  float* lrow = g.logits ? g.logits + (size_t)stream * g.A : nullptr;
+  float* lrow = g.logits ? g.logits + (size_t)stream * A : nullptr;
+  const bool pre_noise = noise_col >= 0 && mode == FW_SAMPLE_GUMBEL;
   float best = -INFINITY, mx = -INFINITY;
-  int bi = g.A;
+  int bi = A;
 #pragma unroll 1
   for (int cc = 0; cc < HALF / 32; ++cc) {
-    float v[32], gn[32];
-    tmem_ld32(trow + cbase + 32 * cc, v);
-    if (noise_col >= 0 && g.mode == FW_SAMPLE_GUMBEL) tmem_ld32(trow + noise_col + cbase + 32 * cc, gn);
-    tmem_wait_ld();
+    float vg[64];  // logits | noise
+    float* v = vg;
+    const float* gn = vg + 32;
+    if (pre_noise)
+      tmem_ld32x2(trow + cbase + 32 * cc, trow + noise_col + cbase + 32 * cc, vg);
+    else
+      tmem_ld32(trow + cbase + 32 * cc, *reinterpret_cast<float(*)[32]>(vg));
+    const float4* b4 = reinterpret_cast<const float4*>(bias + cbase + 32 * cc);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float4 b = __ldg(b4 + q);
+      v[4 * q] += b.x;
+      v[4 * q + 1] += b.y;
+      v[4 * q + 2] += b.z;
+      v[4 * q + 3] += b.w;
+    }
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const int col = cbase + 32 * cc + i;
-      v[i] += __ldg(g.bias + col);
       mx = fmaxf(mx, v[i]);
       float sc = v[i];
-      if (g.mode == FW_SAMPLE_GUMBEL)
-        sc = v[i] + (noise_col >= 0 ? gn[i] : gumbel_noise(prefix, col));
+      if (mode == FW_SAMPLE_GUMBEL) sc = v[i] + (pre_noise ? gn[i] : gumbel_noise(prefix, col));
       if (sc > best) {
         best = sc;
         bi = col;
@@ -708,6 +721,8 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.S = S;
   ca.SK = tc->SK;
   ca.heads = tc->heads;
+  // pair mode: a 2-CTA cluster per tile pair (S = H = 512, A = 256, cluster launch)
+  ca.pair_mode = tc->heads && S == 512 && H == 512 && d.A == 256 && !getenv("FW_NO_CLUSTER");
   ca.H = H;
   ca.sflag = tc->zflag + npairs_all;
   ca.hflag = tc->zflag + 2 * npairs_all;
@@ -779,8 +794,25 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
       ca.sel.next_inputs = (1 < ca.sel.n_inputs) ? ca.sel.inputs + B : nullptr;
       e = cudaMemsetAsync(tc->zflag, 0, sizeof(uint32_t) * 4 * npairs_all, st);
       if (e != cudaSuccess) return e;
-      e = cudaLaunchCooperativeKernel((const void*)step_kernel, dim3(grid), dim3(kChainThreads),
-                                      kargs, kChainSmem, st);
+      {
+        // cooperative (all blocks co-resident: the tail blocks wait on the chain blocks) and
+        // clustered in pairs (a tile pair's two tail blocks share distributed shared memory)
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kChainThreads);
+        cfg.dynamicSmemBytes = kChainSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeCooperative;
+        at[0].val.cooperative = 1;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = 2;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = getenv("FW_NO_CLUSTER") ? 1 : 2;
+        e = cudaLaunchKernelExC(&cfg, (const void*)step_kernel, kargs);
+      }
       if (e != cudaSuccess) return e;
     }
     if (timed) {

@@ -64,13 +64,17 @@ constexpr uint32_t kOffA0 = 0, kOffA1 = kOffA0 + kStageA, kOffB = kOffA1 + kStag
 // then barriers and the selection exchange buffer (4 KB)
 constexpr uint32_t kSkipStage = 2 * kTile + 65536;
 constexpr uint32_t kSkipBars = 2 * kSkipStage;
+constexpr uint32_t kImgBytes = 8 * kTile;  // pair mode: the resident s / h image (128 KB)
+constexpr uint32_t kWStage = 32768;        // pair mode: one head weight K-chunk (256 rows)
+constexpr int kWStages = 3;                // pair mode: head weight ring depth
+constexpr uint32_t kPairBars = kImgBytes + kWStages * kWStage;  // 224 KB
 constexpr uint32_t kTailStage = 2 * (kTile + 32768);  // 2 K-chunks of A | 2 of B (N <= 256)
 constexpr int kTailStages = 2;
 // chain role: after its barriers, two 16 KB staging buffers for popped ring slots
 constexpr uint32_t kOffXq = kOffBars + 1024;
-constexpr size_t kChainSmem = 1024 + (kOffXq + 2 * kSlotBytes > kSkipBars + 8448
-                                          ? kOffXq + 2 * kSlotBytes
-                                          : kSkipBars + 8448);
+constexpr size_t kSmemMax3(size_t a, size_t b, size_t c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+constexpr size_t kChainSmem =
+    1024 + kSmemMax3(kOffXq + 2 * kSlotBytes, kSkipBars + 8448, kPairBars + 256);
 
 // z stash row base of (tile, layer): [tile pair][L][16 pieces][128 rows][16 B]
 __device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int L, int l) {
@@ -289,6 +293,7 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
         if (warp == 2 && lane == 0) {
           red_release_gpu(a.cls_ready + p, 1u);
           trace_g(a, k == 0, 6);
+          if (i == a.n_steps - 2) trace_g(a, k == 0, 17);
         }
       }
     }
@@ -326,6 +331,235 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+// ---- tail role, pair mode (S = H = 512, the two blocks of a tile pair form a 2-CTA
+// cluster): as skip_role, but the pair exchanges its halves of s and h through distributed
+// shared memory instead of global memory + flags. Each block writes its half of s into its
+// own A image and bulk-copies it into the peer's; both run head1 (256 columns of h each)
+// with A resident and only W1 streamed; block 1 sends its half of h into block 0's image
+// once block 0's head1 has released it; block 0 runs head2 and the selection rule.
+__device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem, int k) {
+  const int p = k >> 1, e = k & 1;  // e == cluster rank
+  const int L = a.L, S = a.S, H = a.H;
+  const int ks = S / 64, kh = H / 64;
+  const uint32_t peer = (uint32_t)(e ^ 1);
+  // smem: skip ring [0,192K) while the chain runs; then the s / h image [0,128K) and the
+  // head weight ring [128K,224K); barriers at 224K. The selection's exchange buffer aliases
+  // ring stage 0 (idle once head2's MMAs are complete).
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPairBars);
+  uint64_t* full = bars;           // [2] skip ring
+  uint64_t* empty = bars + 2;      // [2]
+  uint64_t* acc_full = bars + 4;   // skip sum complete (once per step)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 5);
+  uint64_t* wfull = bars + 6;      // [3] head weight ring: one 32 KB K-chunk per stage
+  uint64_t* wempty = bars + 9;     // [3]
+  uint64_t* tacc = bars + 12;      // head accumulator complete (block 0: 2 per step, 1: 1)
+  uint64_t* own_ready = bars + 13; // 256: own half of the image written (+ TMEM read out)
+  uint64_t* peer_full = bars + 14; // tx: the peer's half arrived (block 0: s, h; 1: s)
+  uint64_t* a_free = bars + 15;    // block 1: block 0's image may take h (remote arrive)
+  uint64_t* noise_ready = bars + 16;  // 128: Gumbel noise in TMEM [256,512)
+  uint8_t* img = smem;                 // [8 K-chunks][16 KB]: s, then (block 0) h
+  uint8_t* wring = smem + kImgBytes;   // kWStages x 32 KB
+  float* xch = reinterpret_cast<float*>(wring);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool sel_block = e == 0;
+  const uint32_t half_bytes = 4 * kTile;  // 256 columns x 128 rows fp16
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 13; ++i) mbar_init(bars + i, 1);
+    mbar_init(own_ready, 256);
+    mbar_init(peer_full, 1);
+    mbar_init(a_free, 1);
+    mbar_init(noise_ready, 128);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(peer_full, half_bytes);  // armed before the peer can send
+  }
+  if (warp == 1) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync();  // both blocks' barriers exist and are armed before any exchange
+  const uint32_t tmem = *tmem_holder;
+  const int nw = ks + (sel_block ? kh : 0);  // head weight chunks per step
+  // head weight stream: K-chunk sequence of a step, own half of the image first (head1: W1
+  // rows [256e, 256e+256) chunks 4e.., 4e+1.., head2: W2 chunks 0..7), one 32 KB chunk per
+  // ring stage; stage st is owned by producer thread st (warps 0, 11, 12), so three copies
+  // are in flight
+  auto chunk_of = [&](int j) { return j < ks ? (4 * e + j) % ks : j - ks; };
+  auto head_loads = [&](int step, int owner) {
+    mbar_wait(acc_full, (uint32_t)step & 1);  // the skip ring (same smem) is idle
+    for (int j = 0; j < nw; ++j) {
+      const int J = step * nw + j, st = J % kWStages;
+      if (st != owner) continue;
+      mbar_wait(wempty + st, ((uint32_t)(J / kWStages) & 1) ^ 1);
+      const int c = chunk_of(j);
+      const uint8_t* src = j < ks ? a.wh1b + ((size_t)e * ks + c) * kWStage
+                                  : a.wh2 + (size_t)c * kWStage;
+      mbar_arrive_expect_tx(wfull + st, kWStage);
+      bulk_g2s(wring + st * kWStage, src, kWStage, wfull + st);
+    }
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int i = 0; i < a.n_steps; ++i) {
+        for (int l = 0; l < L; ++l) {
+          const int g = i * L + l, st = g & 1;
+          mbar_wait(empty + st, ((uint32_t)(g >> 1) & 1) ^ 1);
+          wait_counter(a.zflag + p, 2u * (uint32_t)(g + 1));
+          if (l == L - 1) trace_g(a, k == 0, 2);
+          fence_proxy_async_all();
+          uint8_t* stage = smem + st * kSkipStage;
+          mbar_arrive_expect_tx(full + st, 2 * kTile + 65536);
+          bulk_g2s(stage, a.zimg + ((size_t)p * L + l) * 2 * kTile, 2 * kTile, full + st);
+          bulk_g2s(stage + 2 * kTile, a.wskip2 + ((size_t)e * L + l) * 65536, 65536, full + st);
+        }
+        head_loads(i, 0);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t s0 = smem_u32(smem), si = smem_u32(img), sw = smem_u32(wring);
+    const uint32_t id = idesc_f16(128, 256);
+    int pf_phase = 0;  // phases of peer_full consumed
+    for (int i = 0; i < a.n_steps; ++i) {
+      for (int l = 0; l < L; ++l) {
+        const int gl = i * L + l, st = gl & 1;
+        mbar_wait(full + st, (uint32_t)(gl >> 1) & 1);
+        tc_fence_after();
+        const uint32_t sa = s0 + st * kSkipStage, sb = sa + 2 * kTile;
+        if (elect_one()) {
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16(tmem, sdesc_plain(sa + c * kTile + kk * 4096, 2048, 128),
+                       sdesc_sw128(sb + c * 256 * 128 + kk * 32), id, (l | c | kk) != 0);
+          mma_commit(empty + st);
+        }
+        __syncwarp();
+      }
+      if (elect_one()) mma_commit(acc_full);
+      __syncwarp();
+      trace_g(a, k == 0 && lane == 0, 7);
+      for (int g = 0; g < (sel_block ? 2 : 1); ++g) {
+        // K order: own half of the image first (its chunks are written here), the peer's
+        // half (arriving through DSMEM) second -- the MMAs start before the exchange ends
+        const int j0 = g == 0 ? 0 : ks, nj = g == 0 ? ks : kh;
+        for (int j = j0; j < j0 + nj; ++j) {
+          const int J = i * nw + j, st = J % kWStages;
+          const int c = chunk_of(j), jj = j - j0;
+          if (jj == 0) {
+            mbar_wait(own_ready, (uint32_t)(2 * i + g) & 1);  // (+ previous accumulator read)
+            tc_fence_after();
+            trace_g(a, k == 0 && lane == 0, 8 + 3 * g);
+          }
+          if (jj == nj / 2) {
+            mbar_wait(peer_full, (uint32_t)pf_phase & 1);
+            ++pf_phase;
+            if (lane == 0) mbar_arrive_expect_tx(peer_full, half_bytes);  // re-arm
+            __syncwarp();
+            tc_fence_after();
+          }
+          mbar_wait(wfull + st, (uint32_t)(J / kWStages) & 1);
+          tc_fence_after();
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              mma_bf16(tmem, sdesc_sw128(si + c * kTile + kk * 32),
+                       sdesc_sw128(sw + st * kWStage + kk * 32), id, (jj | kk) ? 1u : 0u);
+            mma_commit(wempty + st);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) mma_commit(tacc);
+        __syncwarp();
+        trace_g(a, k == 0 && lane == 0, 10 + 3 * g);
+      }
+    }
+  } else if (warp >= 2 && warp < 10) {
+    const int sub = warp & 3, hf = (warp - 2) >> 2;
+    const int r = sub * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
+    const uint32_t si = smem_u32(img);
+    const float* sbias = a.skip_bsum + e * 256;  // this block's columns of s
+    const float* hbias = a.h1_b + e * 256;       // and of h
+    // own half of an image: TMEM accumulator columns [0,256) + bias -> ReLU -> fp16 chunks
+    // 4e .. 4e+3; then (sender) one bulk copy of those 64 KB into the peer's image
+    auto own_half = [&](const float* bias) {
+      epi_relu_image_smem(trow, r, hf * 128, 128, hf * 128, bias, si + (4 * e + 2 * hf) * kTile);
+      fence_proxy_async();  // generic smem writes -> MMA / bulk-copy reads
+      tc_fence_before();
+      mbar_arrive(own_ready);
+    };
+    auto send_half = [&]() {
+      named_bar_sync(1, 256);
+      if (warp == 2 && lane == 0)
+        bulk_s2peer(mapa(img + 4 * e * kTile, peer), img + 4 * e * kTile, half_bytes,
+                    mapa(peer_full, peer));
+    };
+    for (int i = 0; i < a.n_steps; ++i) {
+      mbar_wait(acc_full, (uint32_t)i & 1);
+      tc_fence_after();
+      trace_g(a, k == 0 && warp == 2 && lane == 0, 14);
+      own_half(sbias);  // s
+      send_half();
+      trace_g(a, k == 0 && warp == 2 && lane == 0, 3);
+      // head1 complete: own half of h (this block's s and the peer's s half are dead)
+      mbar_wait(tacc, (uint32_t)(i * (sel_block ? 2 : 1)) & 1);
+      tc_fence_after();
+      trace_g(a, k == 0 && warp == 2 && lane == 0, 15);
+      if (sel_block) {
+        // block 1 may now overwrite chunks 4..7 of this image with its half of h
+        if (warp == 2 && lane == 0) mbar_arrive_remote(mapa(a_free, peer));
+        own_half(hbias);
+        trace_g(a, k == 0 && warp == 2 && lane == 0, 4);
+        mbar_wait(tacc, 1);  // head2 (2i+1 & 1)
+        if (a.sel.mode == FW_SAMPLE_GUMBEL) mbar_wait(noise_ready, (uint32_t)i & 1);
+        tc_fence_after();
+        trace_g(a, k == 0 && warp == 2 && lane == 0, 5);
+        const SelectArgs sel = sel_step(a.sel, a.t0, i);
+        epi_select(trow, r, hf, p * 128 + r, sel, xch, 256);
+        tc_fence_before();
+        named_bar_sync(1, 256);
+        if (warp == 2 && lane == 0) {
+          red_release_gpu(a.cls_ready + p, 1u);
+          trace_g(a, k == 0, 6);
+          if (i == a.n_steps - 2) trace_g(a, k == 0, 17);
+        }
+      } else {
+        own_half(hbias);  // h columns 256..511 into this image's chunks 4..7
+        mbar_wait_cluster(a_free, (uint32_t)i & 1);
+        send_half();
+      }
+    }
+  } else if (warp >= 10 && warp < 14) {
+    const bool noise = sel_block && a.sel.mode == FW_SAMPLE_GUMBEL;
+    const int sub = warp & 3;
+    const int r = sub * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
+    for (int i = 0; i < a.n_steps; ++i) {
+      if (noise) {
+        const uint32_t prefix = noise_prefix(a.sel.seed, (uint32_t)(a.sel.stream_offset + p * 128 + r),
+                                             (uint32_t)(a.t0 + i));
+        if (i > 0) wait_counter(a.cls_ready + p, (uint32_t)i);
+#pragma unroll 1
+        for (int cc = 0; cc < 8; ++cc) {
+          float gn[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) gn[j] = gumbel_noise(prefix, 32 * cc + j);
+          tmem_st32(trow + 256 + 32 * cc, gn);
+        }
+        tc_fence_before();
+        mbar_arrive(noise_ready);
+      }
+      if ((warp == 11 || warp == 12) && lane == 0) head_loads(i, warp - 10);
+      __syncwarp();
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  cluster_sync();  // no DSMEM traffic into a block that has exited
+  if (warp == 1) tmem_dealloc(tmem, 512);
+}
+
 // One launch per step: blocks [0, nchain) run the chain of one 64-stream tile each, blocks
 // [nchain, nchain + nskip) the skip role (when fused; launched cooperatively so that all
 // blocks are co-resident -- the skip blocks wait on the chain blocks).
@@ -333,7 +567,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   if ((int)blockIdx.x >= a.nchain) {
-    skip_role(a, smem, (int)blockIdx.x - a.nchain);
+    if (a.pair_mode)
+      tail_pair_role(a, smem, (int)blockIdx.x - a.nchain);
+    else
+      skip_role(a, smem, (int)blockIdx.x - a.nchain);
     return;
   }
   uint8_t* stA0 = smem + kOffA0;
@@ -670,10 +907,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       if (l == 0) {
         // step i's input class: written by the pair's selection of step i-1
         if (i > 0) wait_counter(a.cls_ready + (tile >> 1), (uint32_t)i);
+        trace_g(a, tr, 16);
         const int c = a.cls[tile * kChainRows + row];
+        if (tr) {
+          asm volatile("" ::"r"(c) : "memory");
+          trace_g(a, true, 19);
+        }
         const float* e = a.embed + (size_t)c * kR + 64 * h + pc;
 #pragma unroll
         for (int j = 0; j < 32; ++j) xv[j] = __float_as_uint(__ldg(e + 2 * j));
+        if (tr) {
+          asm volatile("" ::"r"(xv[0]), "r"(xv[31]) : "memory");
+          trace_g(a, true, 20);
+        }
         tmem_st_16x64b_x32(trow + kP1 + kColX + 64 * h, xv);
       } else {
         mbar_wait(x_full, (uint32_t)gx & 1);
@@ -701,6 +947,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       tc_fence_before();
       mbar_arrive(xt_ready);
       if (tr) trace_at(a, l, T_EPI_XT, clock64());
+      if (l == 0) trace_g(a, tr, 18);
       // gate of N-half hh: this lane's 16 z columns 64hh + 32h + 2j + pc, j < 16
       const float* bd = a.dil_b + (size_t)l * 2 * kD;
 #pragma unroll

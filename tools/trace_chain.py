@@ -64,7 +64,8 @@ def main():
                  "head1 published", "head2 acc seen", "selection done", "skip acc committed",
                  "h1 mma: tmem free", "h1 first stage", "h1 acc committed",
                  "h2 mma: tmem free", "h2 first stage", "h2 acc committed", "epi: skip acc seen",
-                 "epi: h1 acc seen"]
+                 "epi: h1 acc seen", "chain: cls seen", "prev step selection done",
+                 "chain: layer-0 xt ready", "chain: cls loaded", "chain: embedding loaded"]
         print("step timeline (global ns, last step): " + ", ".join(
             f"{n} {(g[i] - g[0]) / 1e3:.2f} us" for i, n in enumerate(names) if g[i]))
     t = t[:L]
