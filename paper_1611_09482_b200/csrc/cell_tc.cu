@@ -231,22 +231,39 @@ __device__ __forceinline__ float gumbel_noise(uint32_t prefix, int cls) {
   return -__logf(-__logf(u));
 }
 
+// ReLU(v + bias[0..32)) -> 16 packed fp16 pairs. The bias (identical for every thread; global
+// or shared memory, hence generic loads) comes in as 8 independent 16-byte loads: scalar
+// loads next to 64 live accumulator values were serialised by the register budget (~2 us
+// per 128-column epilogue).
+__device__ __forceinline__ void relu_pack32(const float (&v)[32], const float* bias, uint32_t (&w)[16]) {
+  const float4* b4 = reinterpret_cast<const float4*>(bias);
+  float4 b[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) b[q] = b4[q];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    w[2 * q] = pack_h2(fmaxf(v[4 * q] + b[q].x, 0.f), fmaxf(v[4 * q + 1] + b[q].y, 0.f));
+    w[2 * q + 1] = pack_h2(fmaxf(v[4 * q + 2] + b[q].z, 0.f), fmaxf(v[4 * q + 3] + b[q].w, 0.f));
+  }
+}
+
 // ReLU(acc + bias) of TMEM columns [c0, c0 + ncols) of row r -> fp16 SW128 image chunks;
 // column c0 + j is global column n0 + j, in chunk (n0 + j) / 64 of the tile's images at img.
 __device__ __forceinline__ void epi_relu_image(uint32_t trow, int r, int c0, int ncols, int n0,
                                                const float* bias, uint8_t* img) {
-  for (int cc = 0; cc < ncols / 64; ++cc) {
-    float v[64];
-    tmem_ld64(trow + c0 + 64 * cc, v);
-    const int n = n0 + 64 * cc;
-#pragma unroll
-    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + bias[n + i], 0.f);
+#pragma unroll 1
+  for (int cc = 0; cc < ncols / 32; ++cc) {
+    float v[32];
+    uint32_t w[16];
+    tmem_ld32(trow + c0 + 32 * cc, v);
+    const int n = n0 + 32 * cc;
+    relu_pack32(v, bias + n, w);
     uint8_t* dst = img + (size_t)(n / 64) * kTile;
+    const int p0 = (n & 63) / 8;
 #pragma unroll
-    for (int p = 0; p < 8; ++p)
-      *reinterpret_cast<uint4*>(dst + swz(r, p)) =
-          make_uint4(pack_h2(v[8 * p], v[8 * p + 1]), pack_h2(v[8 * p + 2], v[8 * p + 3]),
-                     pack_h2(v[8 * p + 4], v[8 * p + 5]), pack_h2(v[8 * p + 6], v[8 * p + 7]));
+    for (int p = 0; p < 4; ++p)
+      *reinterpret_cast<uint4*>(dst + swz(r, p0 + p)) =
+          make_uint4(w[4 * p], w[4 * p + 1], w[4 * p + 2], w[4 * p + 3]);
   }
 }
 
@@ -254,17 +271,17 @@ __device__ __forceinline__ void epi_relu_image(uint32_t trow, int r, int c0, int
 // sdst + j * 16 KB), bank-conflict free through the swizzle; the caller bulk-stores it.
 __device__ __forceinline__ void epi_relu_image_smem(uint32_t trow, int r, int c0, int ncols,
                                                     int n0, const float* bias, uint32_t sdst) {
-  for (int cc = 0; cc < ncols / 64; ++cc) {
-    float v[64];
-    tmem_ld64(trow + c0 + 64 * cc, v);
-    const int n = n0 + 64 * cc;
+#pragma unroll 1
+  for (int cc = 0; cc < ncols / 32; ++cc) {
+    float v[32];
+    uint32_t w[16];
+    tmem_ld32(trow + c0 + 32 * cc, v);
+    relu_pack32(v, bias + n0 + 32 * cc, w);
+    const uint32_t dst = sdst + (uint32_t)(cc >> 1) * kTile;
+    const int p0 = (cc & 1) * 4;
 #pragma unroll
-    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + bias[n + i], 0.f);
-    const uint32_t dst = sdst + (uint32_t)cc * kTile;
-#pragma unroll
-    for (int p = 0; p < 8; ++p)
-      st_shared_v4(dst + swz(r, p), pack_h2(v[8 * p], v[8 * p + 1]), pack_h2(v[8 * p + 2], v[8 * p + 3]),
-                   pack_h2(v[8 * p + 4], v[8 * p + 5]), pack_h2(v[8 * p + 6], v[8 * p + 7]));
+    for (int p = 0; p < 4; ++p)
+      st_shared_v4(dst + swz(r, p0 + p), w[4 * p], w[4 * p + 1], w[4 * p + 2], w[4 * p + 3]);
   }
 }
 
@@ -272,52 +289,124 @@ __device__ __forceinline__ void epi_relu_image_smem(uint32_t trow, int r, int c0
 // the classes, then the selection rule; the 256 epilogue threads exchange per-row partials
 // through xch ([4][2][128] words, bar.sync 1, 256).
 // noise_col >= 0: the Gumbel noise of the row's classes was precomputed into TMEM columns
-// noise_col + class (fused tail); otherwise it is hashed here.
+// noise_col + class (fused tail); otherwise it is hashed here. add_has_bias: those columns
+// hold bias + noise (Gumbel) or the bias alone (other modes), so no bias loads are needed.
 __device__ __forceinline__ void epi_select(uint32_t trow, int r, int h, int stream,
-                                        const SelectArgs& g, float* xch, int noise_col = -1) {
+                                        const SelectArgs& g, float* xch, int noise_col = -1,
+                                        bool add_has_bias = false, const ChainArgs* tra = nullptr) {
   const int HALF = g.A / 2, A = g.A, mode = g.mode;
-  const float* __restrict__ bias = g.bias;
+  const float* bias = g.bias;
   const uint32_t prefix = noise_prefix(g.seed, (uint32_t)(g.stream_offset + stream), (uint32_t)g.t);
   const int cbase = h * HALF;
   float* lrow = g.logits ? g.logits + (size_t)stream * A : nullptr;
+  const bool tm_add = noise_col >= 0 && add_has_bias;
   const bool pre_noise = noise_col >= 0 && mode == FW_SAMPLE_GUMBEL;
   float best = -INFINITY, mx = -INFINITY;
   int bi = A;
+  if (tm_add) {
+    // x = acc + (bias + noise): the score (Gumbel) or the logit (other modes), one pass with
+    // no memory traffic. Four independent running maxima (a single compare-select chain is
+    // latency-bound), merged lowest index first on ties; mx (inverse CDF) is the max logit.
 #pragma unroll 1
-  for (int cc = 0; cc < HALF / 32; ++cc) {
-    float vg[64];  // logits | noise
-    float* v = vg;
-    const float* gn = vg + 32;
-    if (pre_noise)
-      tmem_ld32x2(trow + cbase + 32 * cc, trow + noise_col + cbase + 32 * cc, vg);
-    else
-      tmem_ld32(trow + cbase + 32 * cc, *reinterpret_cast<float(*)[32]>(vg));
-    const float4* b4 = reinterpret_cast<const float4*>(bias + cbase + 32 * cc);
+    for (int cc = 0; cc < HALF / 32; ++cc) {
+      float x[64];
+      tmem_ld32x2(trow + cbase + 32 * cc, trow + noise_col + cbase + 32 * cc, x);
+      float bv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      int bj[4] = {0, 1, 2, 3};
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const float4 b = __ldg(b4 + q);
-      v[4 * q] += b.x;
-      v[4 * q + 1] += b.y;
-      v[4 * q + 2] += b.z;
-      v[4 * q + 3] += b.w;
-    }
+      for (int i = 0; i < 32; ++i) {
+        const float sc = x[i] + x[32 + i];
+        if (sc > bv[i & 3]) {
+          bv[i & 3] = sc;
+          bj[i & 3] = i;
+        }
+      }
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int col = cbase + 32 * cc + i;
-      mx = fmaxf(mx, v[i]);
-      float sc = v[i];
-      if (mode == FW_SAMPLE_GUMBEL) sc = v[i] + (pre_noise ? gn[i] : gumbel_noise(prefix, col));
-      if (sc > best) {
-        best = sc;
-        bi = col;
+      for (int u = 0; u < 4; ++u) {
+        mx = fmaxf(mx, bv[u]);
+        const int col = cbase + 32 * cc + bj[u];
+        if (bv[u] > best || (bv[u] == best && col < bi)) {
+          best = bv[u];
+          bi = col;
+        }
+      }
+      if (tra && cc < 3) {
+        asm volatile("" ::"f"(best) : "memory");
+        trace_g(*tra, true, 21 + cc);
       }
     }
-    if (lrow) {
-      float4* d4 = reinterpret_cast<float4*>(lrow + cbase + 32 * cc);
+    if (lrow) {  // logits out (acc + bias), a second pass
+#pragma unroll 1
+      for (int cc = 0; cc < HALF / 32; ++cc) {
+        float v[32];
+        tmem_ld32(trow + cbase + 32 * cc, v);
+        const float4* b4 = reinterpret_cast<const float4*>(bias + cbase + 32 * cc);
+        float4* d4 = reinterpret_cast<float4*>(lrow + cbase + 32 * cc);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        for (int q = 0; q < 8; ++q) {
+          const float4 b = __ldg(b4 + q);
+          d4[q] = make_float4(v[4 * q] + b.x, v[4 * q + 1] + b.y, v[4 * q + 2] + b.z, v[4 * q + 3] + b.w);
+        }
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int cc = 0; cc < HALF / 32; ++cc) {
+      float vg[64];  // logits | noise
+      float* v = vg;
+      const float* gn = vg + 32;
+      if (pre_noise)
+        tmem_ld32x2(trow + cbase + 32 * cc, trow + noise_col + cbase + 32 * cc, vg);
+      else
+        tmem_ld32(trow + cbase + 32 * cc, *reinterpret_cast<float(*)[32]>(vg));
+      const float4* b4 = reinterpret_cast<const float4*>(bias + cbase + 32 * cc);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float4 b = __ldg(b4 + q);
+        v[4 * q] += b.x;
+        v[4 * q + 1] += b.y;
+        v[4 * q + 2] += b.z;
+        v[4 * q + 3] += b.w;
+      }
+      // (separate loops: folded into one, the compiler evaluated the noise hash for every
+      // element even when the noise came precomputed)
+      if (pre_noise) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float sc = v[i] + gn[i];
+          if (sc > best) {
+            best = sc;
+            bi = cbase + 32 * cc + i;
+          }
+        }
+      } else if (mode == FW_SAMPLE_GUMBEL) {
+#pragma unroll 4
+        for (int i = 0; i < 32; ++i) {
+          const int col = cbase + 32 * cc + i;
+          const float sc = v[i] + gumbel_noise(prefix, col);
+          if (sc > best) {
+            best = sc;
+            bi = col;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          mx = fmaxf(mx, v[i]);
+          if (v[i] > best) {
+            best = v[i];
+            bi = cbase + 32 * cc + i;
+          }
+        }
+      }
+      if (lrow) {
+        float4* d4 = reinterpret_cast<float4*>(lrow + cbase + 32 * cc);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+      }
     }
   }
+  if (tra) trace_g(*tra, true, 26);
   float* xb = xch;                              // best score  [2][128]
   int* xi = reinterpret_cast<int*>(xch + 256);  // best index [2][128]
   float* xm = xch + 512;                        // max [2][128]
@@ -338,7 +427,7 @@ __device__ __forceinline__ void epi_select(uint32_t trow, int r, int h, int stre
       float v[32];
       tmem_ld32(trow + cbase + 32 * cc, v);
       tmem_wait_ld();
-      for (int i = 0; i < 32; ++i) part += __expf(v[i] + __ldg(g.bias + cbase + 32 * cc + i) - m);
+      for (int i = 0; i < 32; ++i) part += __expf(v[i] + bias[cbase + 32 * cc + i] - m);
     }
     xs[h * 128 + r] = part;
     named_bar_sync(1, 256);
@@ -352,7 +441,7 @@ __device__ __forceinline__ void epi_select(uint32_t trow, int r, int h, int stre
       tmem_ld32(trow + cbase + 32 * cc, v);
       tmem_wait_ld();
       for (int i = 0; i < 32; ++i) {
-        run += __expf(v[i] + __ldg(g.bias + cbase + 32 * cc + i) - m);
+        run += __expf(v[i] + bias[cbase + 32 * cc + i] - m);
         if (found == g.A && run > thr) found = cbase + 32 * cc + i;
       }
     }
@@ -361,6 +450,7 @@ __device__ __forceinline__ void epi_select(uint32_t trow, int r, int h, int stre
     const int f0 = xi[r], f1 = xi[128 + r];
     choice = f0 < g.A ? f0 : (f1 < g.A ? f1 : g.A - 1);
   }
+  if (tra) trace_g(*tra, true, 27);
   if (h == 0) {
     g.out_cls[stream] = choice;
     g.cls_next[stream] = g.next_inputs ? g.next_inputs[stream] : choice;

@@ -68,13 +68,18 @@ constexpr uint32_t kImgBytes = 8 * kTile;  // pair mode: the resident s / h imag
 constexpr uint32_t kWStage = 32768;        // pair mode: one head weight K-chunk (256 rows)
 constexpr int kWStages = 3;                // pair mode: head weight ring depth
 constexpr uint32_t kPairBars = kImgBytes + kWStages * kWStage;  // 224 KB
+// pair mode, after the barriers: biases of s and h (this block's 256 columns each), staged
+// once per launch -- L1 does not keep them (every acquire poll of the flags invalidates it)
+constexpr uint32_t kPairBias = kPairBars + 256;
 constexpr uint32_t kTailStage = 2 * (kTile + 32768);  // 2 K-chunks of A | 2 of B (N <= 256)
 constexpr int kTailStages = 2;
 // chain role: after its barriers, two 16 KB staging buffers for popped ring slots
 constexpr uint32_t kOffXq = kOffBars + 1024;
 constexpr size_t kSmemMax3(size_t a, size_t b, size_t c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
+// No alignment slack: the pair role needs 226.25 KB of the 227. The dynamic window starts
+// 1024-aligned (no static shared memory; the kernel traps otherwise).
 constexpr size_t kChainSmem =
-    1024 + kSmemMax3(kOffXq + 2 * kSlotBytes, kSkipBars + 8448, kPairBars + 256);
+    kSmemMax3(kOffXq + 2 * kSlotBytes, kSkipBars + 8448, kPairBias + 2 * 1024);
 
 // z stash row base of (tile, layer): [tile pair][L][16 pieces][128 rows][16 B]
 __device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int L, int l) {
@@ -343,8 +348,8 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
   const int ks = S / 64, kh = H / 64;
   const uint32_t peer = (uint32_t)(e ^ 1);
   // smem: skip ring [0,192K) while the chain runs; then the s / h image [0,128K) and the
-  // head weight ring [128K,224K); barriers at 224K. The selection's exchange buffer aliases
-  // ring stage 0 (idle once head2's MMAs are complete).
+  // head weight ring [128K,224K); barriers and biases after. The selection's exchange buffer
+  // aliases ring stage 0 (idle once head2's MMAs are complete).
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kPairBars);
   uint64_t* full = bars;           // [2] skip ring
   uint64_t* empty = bars + 2;      // [2]
@@ -360,6 +365,9 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
   uint8_t* img = smem;                 // [8 K-chunks][16 KB]: s, then (block 0) h
   uint8_t* wring = smem + kImgBytes;   // kWStages x 32 KB
   float* xch = reinterpret_cast<float*>(wring);
+  float* sbias = reinterpret_cast<float*>(smem + kPairBias);  // s 256 | h 256
+  for (int c = threadIdx.x; c < 512; c += blockDim.x)
+    sbias[c] = c < 256 ? a.skip_bsum[e * 256 + c] : a.h1_b[e * 256 + c - 256];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool sel_block = e == 0;
   const uint32_t half_bytes = 4 * kTile;  // 256 columns x 128 rows fp16
@@ -403,14 +411,24 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
         for (int l = 0; l < L; ++l) {
           const int g = i * L + l, st = g & 1;
           mbar_wait(empty + st, ((uint32_t)(g >> 1) & 1) ^ 1);
+          // the layer's skip weights do not depend on the chain: in flight before z is --
+          // except in layers 0 and 1, whose stages overlap the previous step's s / h image
+          // and head weight ring until the chain's z (behind that step's selection) says
+          // the heads are done with them
+          uint8_t* stage = smem + st * kSkipStage;
+          const uint8_t* wsrc = a.wskip2 + ((size_t)e * L + l) * 65536;
+          mbar_arrive_expect_tx(full + st, 2 * kTile + 65536);
+          if (l >= 2) bulk_g2s(stage + 2 * kTile, wsrc, 65536, full + st);
           wait_counter(a.zflag + p, 2u * (uint32_t)(g + 1));
           if (l == L - 1) trace_g(a, k == 0, 2);
+          if (l < 2) bulk_g2s(stage + 2 * kTile, wsrc, 65536, full + st);
           fence_proxy_async_all();
-          uint8_t* stage = smem + st * kSkipStage;
-          mbar_arrive_expect_tx(full + st, 2 * kTile + 65536);
           bulk_g2s(stage, a.zimg + ((size_t)p * L + l) * 2 * kTile, 2 * kTile, full + st);
-          bulk_g2s(stage + 2 * kTile, a.wskip2 + ((size_t)e * L + l) * 65536, 65536, full + st);
         }
+        // the step's last acquire in this SM is behind: the logits bias stays in L1 until
+        // the selection reads it
+        if (sel_block)
+          for (int c = 0; c < 1024; c += 128) prefetch_l1(reinterpret_cast<const uint8_t*>(a.sel.bias) + c);
         head_loads(i, 0);
       }
     }
@@ -478,18 +496,21 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
     const int r = sub * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
     const uint32_t si = smem_u32(img);
-    const float* sbias = a.skip_bsum + e * 256;  // this block's columns of s
-    const float* hbias = a.h1_b + e * 256;       // and of h
+    const float* hbias = sbias + 256;
     // own half of an image: TMEM accumulator columns [0,256) + bias -> ReLU -> fp16 chunks
     // 4e .. 4e+3; then (sender) one bulk copy of those 64 KB into the peer's image
+    const bool t2 = k == 0 && warp == 2 && lane == 0;
     auto own_half = [&](const float* bias) {
       epi_relu_image_smem(trow, r, hf * 128, 128, hf * 128, bias, si + (4 * e + 2 * hf) * kTile);
+      trace_g(a, t2, 21);
       fence_proxy_async();  // generic smem writes -> MMA / bulk-copy reads
       tc_fence_before();
       mbar_arrive(own_ready);
+      trace_g(a, t2, 22);
     };
     auto send_half = [&]() {
       named_bar_sync(1, 256);
+      trace_g(a, t2, 23);
       if (warp == 2 && lane == 0)
         bulk_s2peer(mapa(img + 4 * e * kTile, peer), img + 4 * e * kTile, half_bytes,
                     mapa(peer_full, peer));
@@ -511,13 +532,16 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
         own_half(hbias);
         trace_g(a, k == 0 && warp == 2 && lane == 0, 4);
         mbar_wait(tacc, 1);  // head2 (2i+1 & 1)
-        if (a.sel.mode == FW_SAMPLE_GUMBEL) mbar_wait(noise_ready, (uint32_t)i & 1);
+        mbar_wait(noise_ready, (uint32_t)i & 1);
         tc_fence_after();
         trace_g(a, k == 0 && warp == 2 && lane == 0, 5);
         const SelectArgs sel = sel_step(a.sel, a.t0, i);
-        epi_select(trow, r, hf, p * 128 + r, sel, xch, 256);
+        trace_g(a, t2, 28);
+        epi_select(trow, r, hf, p * 128 + r, sel, xch, 256, true, t2 ? &a : nullptr);
+        trace_g(a, t2, 24);
         tc_fence_before();
         named_bar_sync(1, 256);
+        trace_g(a, t2, 25);
         if (warp == 2 && lane == 0) {
           red_release_gpu(a.cls_ready + p, 1u);
           trace_g(a, k == 0, 6);
@@ -530,20 +554,33 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
       }
     }
   } else if (warp >= 10 && warp < 14) {
-    const bool noise = sel_block && a.sel.mode == FW_SAMPLE_GUMBEL;
+    // block 0: TMEM [256,512) of row r <- the logits bias (+ the step's Gumbel noise), added
+    // to the logits by the selection
+    const bool gumbel = a.sel.mode == FW_SAMPLE_GUMBEL;
     const int sub = warp & 3;
     const int r = sub * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(sub * 32) << 16);
     for (int i = 0; i < a.n_steps; ++i) {
-      if (noise) {
+      if (sel_block) {
         const uint32_t prefix = noise_prefix(a.sel.seed, (uint32_t)(a.sel.stream_offset + p * 128 + r),
                                              (uint32_t)(a.t0 + i));
         if (i > 0) wait_counter(a.cls_ready + p, (uint32_t)i);
 #pragma unroll 1
         for (int cc = 0; cc < 8; ++cc) {
           float gn[32];
+          const float4* b4 = reinterpret_cast<const float4*>(a.sel.bias + 32 * cc);
 #pragma unroll
-          for (int j = 0; j < 32; ++j) gn[j] = gumbel_noise(prefix, 32 * cc + j);
+          for (int q = 0; q < 8; ++q) {
+            const float4 b = __ldg(b4 + q);
+            gn[4 * q] = b.x;
+            gn[4 * q + 1] = b.y;
+            gn[4 * q + 2] = b.z;
+            gn[4 * q + 3] = b.w;
+          }
+          if (gumbel) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) gn[j] += gumbel_noise(prefix, 32 * cc + j);
+          }
           tmem_st32(trow + 256 + 32 * cc, gn);
         }
         tc_fence_before();
@@ -565,7 +602,8 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
 // blocks are co-resident -- the skip blocks wait on the chain blocks).
 __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = align1024(smem_raw);
+  if (smem_u32(smem_raw) & 1023u) __trap();  // kChainSmem has no alignment slack
+  uint8_t* smem = smem_raw;
   if ((int)blockIdx.x >= a.nchain) {
     if (a.pair_mode)
       tail_pair_role(a, smem, (int)blockIdx.x - a.nchain);
@@ -913,9 +951,22 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
           asm volatile("" ::"r"(c) : "memory");
           trace_g(a, true, 19);
         }
-        const float* e = a.embed + (size_t)c * kR + 64 * h + pc;
+        // the row's 64 channels 64h.. as 8 float4 loads per lane pair (t, t^2): pair lane pc
+        // loads floats 8q + 4pc .. +3 (one 32-byte sector per pair and load), then each lane
+        // trades the two values of the partner's parity
+        const float4* e4 = reinterpret_cast<const float4*>(a.embed + (size_t)c * kR + 64 * h) + pc;
+        float4 ev[8];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) xv[j] = __float_as_uint(__ldg(e + 2 * j));
+        for (int q = 0; q < 8; ++q) ev[q] = __ldg(e4 + 2 * q);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float s0 = pc ? ev[q].x : ev[q].y, s1 = pc ? ev[q].z : ev[q].w;
+          const float r0 = __shfl_xor_sync(0xffffffffu, s0, 2), r1 = __shfl_xor_sync(0xffffffffu, s1, 2);
+          xv[4 * q] = __float_as_uint(pc ? r0 : ev[q].x);
+          xv[4 * q + 1] = __float_as_uint(pc ? r1 : ev[q].z);
+          xv[4 * q + 2] = __float_as_uint(pc ? ev[q].y : r0);
+          xv[4 * q + 3] = __float_as_uint(pc ? ev[q].w : r1);
+        }
         if (tr) {
           asm volatile("" ::"r"(xv[0]), "r"(xv[31]) : "memory");
           trace_g(a, true, 20);

@@ -86,6 +86,9 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // Warm L2 with [src, src + bytes) (no shared-memory destination, no completion tracking).
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -118,6 +121,11 @@ __device__ __forceinline__ void red_release_gpu(uint32_t* p, uint32_t v) {
   asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v)
                : "memory");
 }
+__device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -128,12 +136,17 @@ __device__ __forceinline__ void fence_proxy_async_all() {
   asm volatile("fence.proxy.async;" ::: "memory");
 }
 // Spin until *p >= target; traps after ~4 s (2^33 cycles) instead of hanging the GPU.
+// Spin until the monotonic counter *p reaches target. The polls are relaxed: every acquire
+// load invalidates the SM's L1 (CCTL.IVALL), which under a polling loop turned other warps'
+// register spills and cached loads into L2 round trips. One acquire load at the end orders
+// the caller's later reads after the release that published the value.
 __device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t target) {
   const long long t0 = clock64();
-  while (ld_acquire_gpu(p) < target) {
+  while (ld_relaxed_gpu(p) < target) {
     __nanosleep(64);
     if (clock64() - t0 > (1ll << 33)) __trap();
   }
+  (void)ld_acquire_gpu(p);
 }
 
 __device__ __forceinline__ long long globaltimer_ns() {

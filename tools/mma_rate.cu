@@ -113,7 +113,7 @@ int main() {
   cudaMalloc(&d, 32);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
   for (int mrows : {64, 128})
-  for (int rot : {8})
+  for (int rot : {8, 0x10008, 0x30008})
   for (int ts = 0; ts < 2; ++ts)
     for (int n : {32, 64, 128, 256}) {
 

@@ -65,7 +65,8 @@ def main():
                  "h1 mma: tmem free", "h1 first stage", "h1 acc committed",
                  "h2 mma: tmem free", "h2 first stage", "h2 acc committed", "epi: skip acc seen",
                  "epi: h1 acc seen", "chain: cls seen", "prev step selection done",
-                 "chain: layer-0 xt ready", "chain: cls loaded", "chain: embedding loaded"]
+                 "chain: layer-0 xt ready", "chain: cls loaded", "chain: embedding loaded",
+                 "sel: cc0 done", "sel: cc1 done", "sel: cc2 done", "sel: epilogue done", "sel: bar", "sel: loop done", "sel: exchange done", "sel: start", "sel: first tmem ld"]
         print("step timeline (global ns, last step): " + ", ".join(
             f"{n} {(g[i] - g[0]) / 1e3:.2f} us" for i, n in enumerate(names) if g[i]))
     t = t[:L]
