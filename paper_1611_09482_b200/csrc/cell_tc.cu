@@ -96,7 +96,7 @@ constexpr int kMaxChainLayers = 128;
 
 // Device-side phase trace (CTA 0 only, clock64 cycles), enabled by fw_debug_trace.
 // Per layer kTraceSlots entries; see tools/trace_chain.py for the slot meanings.
-constexpr int kTraceSlots = 32;
+constexpr int kTraceSlots = 48;
 enum TraceSlot {
   T_MMA_XD = 0, T_MMA_XT, T_MMA_ACC0, T_MMA_ACC1, T_MMA_Z0, T_MMA_Z1, T_MMA_XFULL, T_MMA_WWAIT,
   T_EPI_A, T_EPI_XFULL, T_EPI_XT, T_EPI_ACC0, T_EPI_Z0, T_EPI_ACC1, T_EPI_Z1, T_H0_EARLY,

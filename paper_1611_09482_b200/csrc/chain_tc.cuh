@@ -50,7 +50,7 @@
 // x_full -> next layer's x_{t-d} N-half 1.
 
 constexpr int kChainRows = 64;
-constexpr int kChainThreads = 480;  // 15 warps; 128 registers per thread (4 warps per SMSP)
+constexpr int kChainThreads = 512;  // 16 warps; 128 registers per thread (4 warps per SMSP)
 constexpr int kQueueWarp0 = 10;
 constexpr uint32_t kP1 = 16u << 16;  // lane offset of plane P1
 constexpr uint32_t kColXt = 256, kColXd = 320;  // P0
@@ -636,6 +636,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
   uint64_t* xd_free = bars + 18;   // commit: this layer's x_{t-d} MMAs are done with TMEM xd
   uint64_t* z_stashed = bars + 21;  // 128: queue warps' z stash stores of this layer issued
+  uint64_t* probe = bars + 24;      // [6] trace only: commits after MMA groups (warp 14 stamps)
+  const bool tracing = a.trace != nullptr && blockIdx.x == 0;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tile = blockIdx.x;
@@ -652,6 +654,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     mbar_init(z1_ready, 256);
     mbar_init(xd_free, 1);
     mbar_init(z_stashed, 128);
+    for (int i = 0; i < 6; ++i) mbar_init(probe + i, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
@@ -745,7 +748,10 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       __syncwarp();
       // the gate warps rewrite z after acc0_full: the previous layer's stash has read it
       if (g > 0) mbar_wait(z_read, par ^ 1);
-      if (elect_one()) mma_commit(acc0_full);
+      if (elect_one()) {
+        mma_commit(acc0_full);
+        if (tracing) mma_commit(probe + 0);
+      }
       __syncwarp();
       if (lane == 0) trace_at(a, l, T_MMA_ACC0, clock64());
       if (!early[1]) {
@@ -756,12 +762,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         }
         __syncwarp();
       }
+      if (tracing && elect_one()) mma_commit(probe + 1);
+      __syncwarp();
       early[0] = early[1] = false;
       if (elect_one()) {
         mma_tmem_a(tmem + 128, tmem + kColXt + 0, sb + 2 * kChunk);
         mma_tmem_a(tmem + 128, tmem + kColXt + 32, sb + 3 * kChunk);
         mma_commit(acc1_full);
         mma_commit(emptyB);
+        if (tracing) mma_commit(probe + 2);
       }
       __syncwarp();
       if (lane == 0) trace_at(a, l, T_MMA_ACC1, clock64());
@@ -774,6 +783,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         if (elect_one()) mma_tmem_a(tmem + kP1 + kColX, tmem + kP1 + kColZ + 0, sc + 0 * kChunk);
         __syncwarp();
       }
+      if (tracing && elect_one()) mma_commit(probe + 3);
+      __syncwarp();
       if (nxg) {
         // acc0 is free (gate half 0 done): the next layer's x_{t-d} N-half 0 (the next
         // step's layer 0 included -- it needs no input class). Its operand follows this
@@ -787,6 +798,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         __syncwarp();
         early[0] = true;
       }
+      if (tracing && elect_one()) mma_commit(probe + 4);
+      __syncwarp();
       mbar_wait(z1_ready, par);
       if (lane == 0) trace_at(a, l, T_MMA_Z1, clock64());
       tc_fence_after();
@@ -796,6 +809,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
           mma_commit(emptyC);
         }
         __syncwarp();
+        if (tracing && elect_one()) mma_commit(probe + 5);
+        __syncwarp();
         // the gate warps rewrite xt after x_full: this layer's push has read it
         mbar_wait(x_pushed, par);
         if (elect_one()) mma_commit(x_full);
@@ -804,6 +819,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         if (lane == 0) trace_at(a, l, T_MMA_XFULL, clock64());
         // (x_{t-d} half 1 stays in the layer: issued here it would hold the tensor pipe
         // and this warp when the next layer's x_t MMAs become ready)
+      } else {
+        if (tracing && elect_one()) mma_commit(probe + 5);
+        __syncwarp();
       }
       if (lane == 0) trace_at(a, l, T_MMA_WWAIT, wwait);
     }
@@ -917,6 +935,15 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         mbar_wait(z_stashed, (uint32_t)g & 1);
         red_release_gpu(a.zflag + (tile >> 1), 1u);
       }
+    }
+  } else if (warp == 15) {
+    if (lane == 0 && tracing) {
+      // trace: completion times of the MMA groups (probe commits, in pipe order)
+      for (int g = 0; g < G; ++g)
+        for (int k = 0; k < 6; ++k) {
+          mbar_wait(probe + k, (uint32_t)g & 1);
+          trace_at(a, g % L, 32 + k, clock64());
+        }
     }
   } else if (warp >= 2 && warp < 10) {
     // ---- gate warps: quadrant q, half h; 16x64b accesses: lane t holds row

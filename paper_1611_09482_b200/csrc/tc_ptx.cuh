@@ -117,9 +117,10 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t threads) {
 }
 // Release increment of a global counter: fence.acq_rel.gpu + relaxed red (the pattern of
 // CUTLASS's GenericBarrier); after a CTA barrier it publishes the writes of all its threads.
+// Release-add: publishes everything ordered before it (MEMBAR.GPU + RED). Not a
+// fence.acq_rel: its acquire half invalidates the SM's L1 (CCTL.IVALL) for nothing.
 __device__ __forceinline__ void red_release_gpu(uint32_t* p, uint32_t v) {
-  asm volatile("fence.acq_rel.gpu;\n\tred.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v)
-               : "memory");
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_relaxed_gpu(const uint32_t* p) {
   uint32_t v;

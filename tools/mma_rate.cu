@@ -16,6 +16,7 @@ __global__ void probe(int n, int ts, int count, long long* out, int rot, int mro
   __shared__ uint32_t holder;
   const int warp = threadIdx.x / 32;
   const bool rnd = (rot >> 16) & 1, ldload = (rot >> 17) & 1;
+  const int rot_all = rot;
   rot &= 0xFFFF;
   for (int i = threadIdx.x; i < 65536 / 16; i += blockDim.x) {
     uint32_t x = rnd ? (uint32_t)i * 2654435761u + 12345u : 0u;
@@ -31,7 +32,8 @@ __global__ void probe(int n, int ts, int count, long long* out, int rot, int mro
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = holder;
+  // bit 18 of rot: accumulator and TMEM A operand in plane P1 (lane offset 16, M = 64)
+  const uint32_t tmem = holder + (((rot >> 18) & 1) ? (16u << 16) : 0u);
   const bool elect_mode = rot >= 8;
   __shared__ int stop;
   if (threadIdx.x == 0) stop = 0;
@@ -112,8 +114,8 @@ int main() {
   long long* d;
   cudaMalloc(&d, 32);
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536 + 1024);
-  for (int mrows : {64, 128})
-  for (int rot : {8, 0x10008, 0x30008})
+  for (int mrows : {64})
+  for (int rot : {8, 0x40008})
   for (int ts = 0; ts < 2; ++ts)
     for (int n : {32, 64, 128, 256}) {
 

@@ -23,9 +23,10 @@ from paper_1611_09482_b200 import CellGenerator, Sampler, _lib, build_cell_model
 NAMES = ["mma_xd", "mma_xt", "mma_acc0", "mma_acc1", "mma_z0", "mma_z1", "mma_xful", "mma_wwai",
          "epi_a", "epi_xful", "epi_xt", "epi_acc0", "epi_z0", "epi_acc1", "epi_z1", "h0_early",
          "q_xd", "q_load", "prod_a0", "prod_a1", "prod_b", "prod_c", "g0_ld", "g0_math",
-         "q_xdfree", "q_xqfull", "g1_ld", "g1_math", "q_bar", "q_rel", "q_stash", "q_end"]
+         "q_xdfree", "q_xqfull", "g1_ld", "g1_math", "q_bar", "q_rel", "q_stash", "q_end",
+         "c_xt0", "c_xd1", "c_xt1", "c_resz0", "c_xd0e", "c_resz1"]
 RAW = {7, 15}  # counts / flags, not timestamps
-SLOTS = len(NAMES)
+SLOTS = 48  # kTraceSlots
 
 
 def main():
@@ -50,7 +51,7 @@ def main():
         row = t[l].copy()
         ref = row[8]
         cells = []
-        for i, v in enumerate(row):
+        for i, v in enumerate(row[:len(NAMES)]):
             if i in RAW:
                 cells.append(f"{v:8d}")
             elif v == 0:
