@@ -231,7 +231,8 @@ __device__ __forceinline__ float gumbel_noise(uint32_t prefix, int cls) {
   return -__logf(-__logf(u));
 }
 
-// ReLU(v + bias[0..32)) -> 16 packed fp16 pairs. The bias (identical for every thread; global
+// ReLU(v + bias[0..32)) -> 16 packed fp16 pairs (bias null: none). The bias (identical for
+// every thread; global
 // or shared memory, hence generic loads) comes in as 8 independent 16-byte loads: scalar
 // loads next to 64 live accumulator values were serialised by the register budget (~2 us
 // per 128-column epilogue).
@@ -239,7 +240,7 @@ __device__ __forceinline__ void relu_pack32(const float (&v)[32], const float* b
   const float4* b4 = reinterpret_cast<const float4*>(bias);
   float4 b[8];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) b[q] = b4[q];
+  for (int q = 0; q < 8; ++q) b[q] = bias ? b4[q] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     w[2 * q] = pack_h2(fmaxf(v[4 * q] + b[q].x, 0.f), fmaxf(v[4 * q + 1] + b[q].y, 0.f));
