@@ -21,8 +21,8 @@
 //     P1 [128,192)  z     fp16 z operand of the res MMA
 //   Gate and conversion use 16-lane (16x64b) accesses that touch one plane; the queue warps'
 //   32x32b accesses touch both, and the columns of the other plane under their regions are
-//   scratch. Every MMA takes A from TMEM (an SMEM A operand costs ~107 instead of ~72 cycles
-//   per MMA, tools/mma_latency.cu). SMEM holds only the weight stages A0 / A1 (32 KB each:
+//   scratch. Every MMA takes A from TMEM (the operands are produced there; an SMEM A operand
+//   is no faster inside this kernel, tools/mma_rate.cu). SMEM holds the weight stages A0 / A1 (32 KB each:
 //   the x_{t-d} K-chunks of N-half 0 / 1), B (64 KB: the x_t K-chunks of both halves) and C
 //   (32 KB: res), one bulk copy each per layer (~500 cycles per copy, tools/ring_bw.cu).
 //
@@ -33,6 +33,7 @@
 //   K-major UMMA layout (sdesc_plain); tile 2p fills rows 0..63, tile 2p+1 rows 64..127.
 //
 //   warp 0  lane 0  weight producer (stages A0, A1, B, C in consumption order)
+//   warp 14 lane 0  publisher (z stash release); warp 15: MMA completion watcher (trace only)
 //   warp 1          MMA issuer: the converged warp issues under elect.sync (tools/mma_rate.cu)
 //   warps 2..9      gate warps, quadrant q = warp % 4 (rows 16q..16q+15), half h = (warp-2)/4,
 //                   all accesses 16x64b -- every lane busy: lane t holds row (t>>2) + 8(t&1),
