@@ -119,6 +119,20 @@ int fw_cell_generate_host(fw_handle* h, const int32_t* h_inputs, int32_t n_input
                           int32_t n_steps, int32_t* h_out, const fw_sampler* sampler,
                           void* stream);
 
+/* Full-sequence (time-parallel) forward over T given inputs per stream, from the
+ * handle's current state: leaves the queues and the step counter exactly where T
+ * teacher-forced steps of fw_cell_generate (n_inputs = n_steps = T) would, and writes
+ * the logits of all T steps to d_logits [T][B][A] fp32 (nullable: queues only, the
+ * skip sum and heads are skipped). The analogue of the reference's forward_full /
+ * causal_dilated_conv (streamconv oracle.py:84-123) for the cell, used to prefill the
+ * queues from a long primer (the reference steps primers, fast.py:244-245): the layers
+ * run as GEMMs over all (time, stream) rows of a chunk instead of T dependent steps --
+ * except on tcgen05 handles of >= 2,048 streams, where teacher-forced steps of the fused
+ * step kernel are faster and are used instead (same end state; FW_PREFILL_MODE=gemm|steps
+ * forces either). */
+int fw_cell_prefill(fw_handle* h, const int32_t* d_inputs, int32_t T, float* d_logits,
+                    void* stream);
+
 /* ---- plain mode: the reference's own stack, float64 (model.py, fast.py) ---- */
 
 typedef struct fw_plain_desc {

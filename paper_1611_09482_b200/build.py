@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfastwavenet.so"
-SOURCES = ["capi.cu", "cell_simt.cu", "cell_tc.cu", "plain_f64.cu"]
+SOURCES = ["capi.cu", "cell_simt.cu", "cell_tc.cu", "plain_f64.cu", "prefill.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
     tmp_lib = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), "-shared", "-o", str(tmp_lib), *map(str, objs), *ARCH]
+    cmd = [nvcc(), "-shared", "-o", str(tmp_lib), *map(str, objs), *ARCH, "-ldl"]
     subprocess.run(cmd, check=True)
     os.replace(tmp_lib, LIB)
     return LIB

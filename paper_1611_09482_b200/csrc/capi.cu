@@ -2,6 +2,7 @@
 // weight repacking, queue allocation, argument validation and dispatch.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -71,6 +72,7 @@ void free_cell(Handle& h) {
   h.d_dil = nullptr;
   h.d_qoff = nullptr;
   if (h.tc) tc_destroy(h);
+  prefill_destroy(h);
 }
 
 void free_plain(Handle& h) {
@@ -318,6 +320,38 @@ int fw_cell_generate_host(fw_handle* fh, const int32_t* h_inputs, int32_t n_inpu
                           cudaMemcpyDeviceToHost, st));
   FW_CUDA(cudaStreamSynchronize(st));
   return FW_OK;
+}
+
+int fw_cell_prefill(fw_handle* fh, const int32_t* d_inputs, int32_t T, float* d_logits,
+                    void* stream) {
+  int rc = check_handle(fh, false);
+  if (rc) return rc;
+  if (T < 0) return invalid("T must be non-negative");
+  if (T == 0) return FW_OK;
+  if (!d_inputs) return invalid("d_inputs must not be null");
+  Handle& h = fh->h;
+  FW_CUDA(cudaSetDevice(h.device));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // Two ways to the same end state. Time-parallel GEMMs (prefill.cu) move every layer's
+  // fp32 intermediates through HBM, ~54 ns per (step, stream) for a cfg4-sized model; the
+  // tcgen05 step kernel keeps them on chip and costs ~110 us per step for any batch up to
+  // 4,096 streams. Below ~2,048 streams (and always on the SIMT path, whose steps are
+  // latency-bound) the GEMMs win; above, teacher-forced steps do.
+  // FW_PREFILL_MODE=gemm|steps forces one.
+  const char* mode = getenv("FW_PREFILL_MODE");
+  bool steps = h.kernel == FW_KERNEL_TCGEN05 && h.batch >= 2048;
+  if (mode) steps = std::string(mode) == "steps";
+  if (!steps) return cell_prefill(h, d_inputs, T, d_logits, st);
+  const int64_t need = (int64_t)T * h.batch;
+  if (need > h.d_io_elems) {
+    if (h.d_io) cudaFree(h.d_io);
+    h.d_io = nullptr;
+    h.d_io_elems = 0;
+    FW_CUDA(cudaMalloc(&h.d_io, sizeof(int32_t) * (size_t)need));
+    h.d_io_elems = need;
+  }
+  CellRun run{d_inputs, T, T, h.d_io, d_logits, d_logits ? T : 0, h.t, FW_SAMPLE_ARGMAX, 0u, 0};
+  return run_cell(h, run, st);
 }
 
 int fw_plain_create(const fw_plain_desc* d, int32_t batch, int32_t device, fw_handle** out) {

@@ -901,7 +901,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
         at[1].val.clusterDim.y = 1;
         at[1].val.clusterDim.z = 1;
         cfg.attrs = at;
-        cfg.numAttrs = getenv("FW_NO_CLUSTER") ? 1 : 2;
+        cfg.numAttrs = ca.pair_mode ? 2 : 1;  // the cluster dimension only for the pair tail
         e = cudaLaunchKernelExC(&cfg, (const void*)step_kernel, kargs);
       }
       if (e != cudaSuccess) return e;

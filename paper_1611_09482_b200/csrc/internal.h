@@ -77,6 +77,8 @@ struct SimtWeights {
 
 // tcgen05 path device state (see cell_tc.cu).
 struct TcState;
+// full-sequence prefill state (see prefill.cu).
+struct PrefillState;
 
 struct Handle;
 
@@ -89,6 +91,8 @@ int tc_create(Handle& h, const fw_cell_desc* desc);
 void tc_destroy(Handle& h);
 void tc_set_trace(Handle& h, long long* trace);
 int64_t tc_debug_buffer(Handle& h, int which, const void** src);
+int cell_prefill(Handle& h, const int32_t* d_inputs, int T, float* d_logits, cudaStream_t st);
+void prefill_destroy(Handle& h);
 
 struct PlainDev {
   int n_layers, w, act;
@@ -132,6 +136,7 @@ struct Handle {
   int64_t queue_bytes = 0;
   SimtWeights w{};
   TcState* tc = nullptr;
+  PrefillState* prefill = nullptr;
 
   // plain
   PlainDev p{};

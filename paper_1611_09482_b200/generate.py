@@ -169,6 +169,25 @@ class CellGenerator:
             int(n_logit_steps), C.byref(s), _lib.stream_ptr(stream)))
         return out, (logits if n_logit_steps else None)
 
+    def prefill(self, inputs, want_logits: bool = False, logits=None, stream=None):
+        """Full-sequence forward over given inputs (T, B) int32 on the GPU
+        (fw_cell_prefill): the queues and the step counter end where T teacher-forced
+        steps would leave them, computed time-parallel. Returns the logits (T, B, A) of
+        every step when asked for, else None."""
+        import torch
+
+        x = self._i32(inputs)
+        if x.dim() != 2 or x.shape[1] != self.batch:
+            raise ValueError("inputs must have shape (T, batch)")
+        T = int(x.shape[0])
+        if want_logits and logits is None:
+            logits = torch.empty((T, self.batch, self.config.classes), dtype=torch.float32,
+                                 device=self._dev)
+        _lib.check(self._lib.fw_cell_prefill(
+            self._h, C.c_void_p(x.data_ptr()), T,
+            C.c_void_p(logits.data_ptr() if want_logits else 0), _lib.stream_ptr(stream)))
+        return logits if want_logits else None
+
     def generate_host(self, inputs: np.ndarray, n_steps: int, sampler: Sampler = Sampler(),
                       out: np.ndarray | None = None, stream=None) -> np.ndarray:
         """Host in, host out: the end-to-end C-ABI entry (fw_cell_generate_host)."""

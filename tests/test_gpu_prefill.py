@@ -1,0 +1,145 @@
+"""GPU full-sequence forward (fw_cell_prefill) against teacher-forced
+stepping and the CPU oracle's forward_full (the reference's full-sequence ground truth,
+oracle.py:84-123, restated for the cell).
+
+The prefill must leave the handle exactly where T teacher-forced steps leave it: same step
+counter, the same ring contents (every layer's last d_l inputs), and the same logits for
+every step -- so generation continues identically. Tolerances: fp32 configs (SIMT handles,
+fp32 GEMMs without TF32) 1e-4 max-abs on logits; bf16 configs (tcgen05 handles, fp16
+operands) the north star's 2e-2.
+"""
+
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cell as oc
+from paper_1611_09482_b200 import CellGenerator, Sampler, build_cell_model
+from paper_1611_09482_b200.cell import CellConfig
+
+pytestmark = pytest.mark.gpu
+
+SIMT_CFG = CellConfig(1, 10, 32, 32, 128, init="normal:0.1", bias="fan_in", init_seed=3)
+TC_CFG = CellConfig(2, 4, 128, 128, 256, weight_dtype="bf16", bias="fan_in", init_seed=5)
+CASES = {"simt": (SIMT_CFG, 3, 1e-4), "tcgen05": (TC_CFG, 128, 2e-2)}
+
+
+@pytest.fixture(scope="module")
+def models():
+    return {k: build_cell_model(c) for k, (c, _, _) in CASES.items()}
+
+
+def teacher(T, B, seed, A=256):
+    return np.random.default_rng(seed).integers(0, A, (T, B)).astype(np.int32)
+
+
+def queue_values(gen):
+    """The handle's ring contents as floats (fp32 SIMT slots, fp16 tcgen05 slots)."""
+    nbytes = gen.queue_bytes
+    buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    from paper_1611_09482_b200 import _lib
+    import ctypes as C
+
+    _lib.check(gen._lib.fw_debug_copy(gen._h, 0, C.c_void_p(buf.data_ptr()), nbytes, None))
+    torch.cuda.synchronize()
+    dt = torch.float16 if gen.kernel == "tcgen05" else torch.float32
+    return buf.view(dt).float().cpu().numpy()
+
+
+def stepped(model, kernel, B, x):
+    gen = CellGenerator(model, B, kernel=kernel)
+    _, lg = gen.generate(torch.as_tensor(x, device="cuda"), x.shape[0], Sampler(0),
+                         n_logit_steps=x.shape[0])
+    torch.cuda.synchronize()
+    return gen, lg.cpu().numpy()
+
+
+@pytest.mark.parametrize("kernel", ["simt", "tcgen05"])
+@pytest.mark.parametrize("T", [1, 37, 300])
+def test_prefill_matches_teacher_forced_steps(cuda, models, kernel, T):
+    cfg, B, tol = CASES[kernel]
+    x = teacher(T, B, 11 + T)
+    ref_gen, ref = stepped(models[kernel], kernel, B, x)
+    gen = CellGenerator(models[kernel], B, kernel=kernel)
+    lg = gen.prefill(torch.as_tensor(x, device="cuda"), want_logits=True)
+    torch.cuda.synchronize()
+    assert gen.step_index == T == ref_gen.step_index
+    dev = np.max(np.abs(lg.cpu().numpy() - ref))
+    assert dev <= tol, dev
+    qd = np.max(np.abs(queue_values(gen) - queue_values(ref_gen)))
+    assert qd <= (1e-4 if kernel == "simt" else 2e-2), qd
+
+
+@pytest.mark.parametrize("kernel", ["simt", "tcgen05"])
+def test_prefill_against_oracle_forward_full(cuda, models, kernel):
+    cfg, B, tol = CASES[kernel]
+    T = 200
+    x = teacher(T, B, 99)
+    gen = CellGenerator(models[kernel], B, kernel=kernel)
+    lg = gen.prefill(torch.as_tensor(x, device="cuda"), want_logits=True).cpu().numpy()
+    o = oc.CellOracle(models[kernel])
+    for b in sorted({0, B - 1}):
+        ref = o.forward_full(x[:, b])
+        dev = np.max(np.abs(lg[:, b] - ref))
+        assert dev <= tol, (b, dev)
+
+
+@pytest.mark.parametrize("kernel", ["simt", "tcgen05"])
+def test_prefill_then_generation_continues(cuda, models, kernel):
+    """Queues only (no logits), from a non-zero step, in two calls, then teacher-forced
+    steps: the continuation's logits match an all-stepped run."""
+    cfg, B, tol = CASES[kernel]
+    x = teacher(150, B, 7)
+    head, p1, p2, tail = x[:9], x[9:80], x[80:120], x[120:]
+    ref_gen, ref = stepped(models[kernel], kernel, B, x)
+    gen = CellGenerator(models[kernel], B, kernel=kernel)
+    gen.generate(torch.as_tensor(head, device="cuda"), len(head), Sampler(0))
+    assert gen.prefill(torch.as_tensor(p1, device="cuda")) is None
+    gen.prefill(torch.as_tensor(p2, device="cuda"))
+    assert gen.step_index == 120
+    _, lg = gen.generate(torch.as_tensor(tail, device="cuda"), len(tail), Sampler(0),
+                         n_logit_steps=len(tail))
+    torch.cuda.synchronize()
+    dev = np.max(np.abs(lg.cpu().numpy() - ref[120:]))
+    assert dev <= tol, dev
+
+
+@pytest.mark.parametrize("kernel", ["simt", "tcgen05"])
+def test_prefill_chunking_invariance(cuda, models, kernel, monkeypatch):
+    cfg, B, tol = CASES[kernel]
+    x = teacher(90, B, 5)
+    outs = []
+    for chunk in (1, 7, 90):
+        monkeypatch.setenv("FW_PREFILL_CHUNK", str(chunk))
+        gen = CellGenerator(models[kernel], B, kernel=kernel)
+        outs.append((gen.prefill(torch.as_tensor(x, device="cuda"), want_logits=True).cpu().numpy(),
+                     queue_values(gen)))
+    for lg, q in outs[1:]:
+        assert np.max(np.abs(lg - outs[0][0])) <= tol / 10
+        assert np.max(np.abs(q - outs[0][1])) <= (1e-5 if kernel == "simt" else 2e-3)
+
+
+def test_prefill_argument_errors(cuda, models):
+    gen = CellGenerator(models["simt"], 3, kernel="simt")
+    with pytest.raises(ValueError):
+        gen.prefill(torch.zeros((4, 2), dtype=torch.int32, device="cuda"))
+    assert gen.prefill(torch.zeros((0, 3), dtype=torch.int32, device="cuda")) is None
+    assert gen.step_index == 0
+
+
+def test_prefill_modes_agree(cuda, models, monkeypatch):
+    """The two implementations behind fw_cell_prefill (time-parallel GEMMs, teacher-forced
+    steps of the fused kernel) leave the same state and logits."""
+    cfg, B, tol = CASES["tcgen05"]
+    x = teacher(64, B, 21)
+    res = {}
+    for mode in ("gemm", "steps"):
+        monkeypatch.setenv("FW_PREFILL_MODE", mode)
+        gen = CellGenerator(models["tcgen05"], B, kernel="tcgen05")
+        lg = gen.prefill(torch.as_tensor(x, device="cuda"), want_logits=True).cpu().numpy()
+        res[mode] = (lg, queue_values(gen), gen.step_index)
+    assert res["gemm"][2] == res["steps"][2] == 64
+    assert np.max(np.abs(res["gemm"][0] - res["steps"][0])) <= tol
+    assert np.max(np.abs(res["gemm"][1] - res["steps"][1])) <= 2e-2
