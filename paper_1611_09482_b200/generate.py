@@ -208,14 +208,20 @@ def init_cell_state(model: CellModel, batch: int = 1, device: int | None = None,
     return CellGenerator(model, batch, device, kernel)
 
 
+PREFILL_MIN_PRIMER = 64  # primers at least this long run their phase time-parallel
+
+
 def cell_fast_generate(model: CellModel, primer, steps: int, batch: int | None = None,
                        sampler: Sampler = Sampler(), device: int | None = None,
-                       kernel: str = "auto") -> np.ndarray:
+                       kernel: str = "auto", prefill_primer: bool = True) -> np.ndarray:
     """fast_generate for class streams; returns generated classes (B, steps).
 
     ``primer`` is (P,) shared by all streams or (B, P); an empty primer is the
     single class 0 (the reference's empty-primer rule, oracle.py:65-81, with the
-    zero sample as class 0).
+    zero sample as class 0). The reference steps primer[:-1] with the outputs
+    discarded (fast.py:244-245); from PREFILL_MIN_PRIMER samples on (and with
+    ``prefill_primer``) that phase is the time-parallel full-sequence forward
+    (fw_cell_prefill), which leaves the same state.
     """
     if steps < 0:
         raise ValueError("steps must be non-negative")
@@ -232,6 +238,14 @@ def cell_fast_generate(model: CellModel, primer, steps: int, batch: int | None =
         return np.zeros((B, 0), dtype=np.int32)
     P = p.shape[1]
     gen = CellGenerator(model, B, device, kernel)
+    if prefill_primer and P - 1 >= PREFILL_MIN_PRIMER:
+        import torch
+
+        gen.prefill(torch.as_tensor(np.ascontiguousarray(p[:, :-1].T), dtype=torch.int32,
+                                    device=gen._dev))
+        out = gen.generate_host(np.ascontiguousarray(p[:, -1:].T), steps, sampler)
+        gen.close()
+        return np.ascontiguousarray(out.T)
     out = gen.generate_host(np.ascontiguousarray(p.T), P - 1 + steps, sampler)
     gen.close()
     return np.ascontiguousarray(out[P - 1:].T)
