@@ -241,7 +241,7 @@ def cell_fast_generate(model: CellModel, primer, steps: int, batch: int | None =
     if prefill_primer and P - 1 >= PREFILL_MIN_PRIMER:
         import torch
 
-        gen.prefill(torch.as_tensor(np.ascontiguousarray(p[:, :-1].T), dtype=torch.int32,
+        gen.prefill(torch.as_tensor(np.array(p[:, :-1].T, dtype=np.int32), dtype=torch.int32,
                                     device=gen._dev))
         out = gen.generate_host(np.ascontiguousarray(p[:, -1:].T), steps, sampler)
         gen.close()
