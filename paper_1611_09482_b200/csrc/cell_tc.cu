@@ -38,7 +38,7 @@ struct TcState {
   uint8_t* wchain = nullptr;  // per layer: 10 chunks [128][64] in MMA issue order
   uint8_t* wskip = nullptr;   // [S/128][L*D/64] chunks of [128][64] (unfused skip GEMM)
   uint8_t* wskip2 = nullptr;  // [S/SK][L][2][SK][64] (fused skip role of the step kernel)
-  uint32_t* zflag = nullptr;  // [4][B/128] fused counters: z stash | s | h | selections
+  uint32_t* zflag = nullptr;  // [5][B/128] fused counters: z stash | s | h | selections | z reads
   int64_t* d_qoff = nullptr;  // [L] byte offset of each layer's ring
   int fused = 0, SK = 256, nchain = 0, nskip = 0;
   int heads = 0;              // head1 / head2 fused into the skip blocks (needs fused)
@@ -153,6 +153,9 @@ struct ChainArgs {
   // fused skip role (zflag != null): blocks >= nchain accumulate the skip sum
   int nchain;
   uint32_t* zflag;         // [B/128] per tile pair: chain tiles x layers stashed so far
+  int zring;               // layers in the z stash ring (slot = global layer index % zring)
+  uint32_t* zfree;         // [B/128] per tile pair: z tiles read by the tail blocks, or null
+  int ztail;               // tail blocks per pair (reads per z tile)
   uint32_t* cls_ready;     // [B/128] per tile pair: steps whose selection is written
   const uint8_t* wskip2;   // [S/SK][L][2 K-chunks][SK rows][128 B]
   const float* skip_bsum;  // [S]
@@ -712,7 +715,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
           pack_image(img.data() + (((size_t)e * L + l) * 2 + c) * SK * 128, SK, c * 64,
                      [&](int n, int k) { return desc->skip_w[((size_t)l * S + e * SK + n) * kD + k]; });
     if (int rc = upload_bytes(&tc->wskip2, img)) return rc;
-    if (int rc = dev_alloc(&tc->zflag, sizeof(uint32_t) * 4 * (h.batch / 128))) return rc;
+    if (int rc = dev_alloc(&tc->zflag, sizeof(uint32_t) * 5 * (h.batch / 128))) return rc;
     // ring offsets: layer l's d_l slots follow the earlier layers', each slot holds every tile
     std::vector<int64_t> qoff(L);
     for (int l = 0, acc = 0; l < L; ++l) {
@@ -806,6 +809,10 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   const int npairs_all = B / 128;
   ca.nchain = B / kChainRows;
   ca.zflag = tc->fused ? tc->zflag : nullptr;
+  // z stash: a 16-layer ring per pair in the fused kernel (the unfused skip GEMM reads all L)
+  ca.zring = tc->fused ? std::min(L, 16) : L;
+  ca.zfree = tc->fused ? tc->zflag + 4 * npairs_all : nullptr;
+  ca.ztail = tc->nskip / npairs_all;  // tail blocks per pair, each reads every z tile
   ca.wskip2 = tc->wskip2;
   ca.skip_bsum = tc->skip_bsum;
   ca.simg = tc->simg;
@@ -883,7 +890,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
       ca.sel.out_cls = ca.sel.out_base;
       ca.sel.logits = (run.logits && i0 < run.n_logit_steps) ? ca.sel.logits_base : nullptr;
       ca.sel.next_inputs = (1 < ca.sel.n_inputs) ? ca.sel.inputs + B : nullptr;
-      e = cudaMemsetAsync(tc->zflag, 0, sizeof(uint32_t) * 4 * npairs_all, st);
+      e = cudaMemsetAsync(tc->zflag, 0, sizeof(uint32_t) * 5 * npairs_all, st);
       if (e != cudaSuccess) return e;
       {
         // cooperative (all blocks co-resident: the tail blocks wait on the chain blocks) and

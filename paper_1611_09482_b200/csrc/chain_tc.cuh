@@ -80,10 +80,22 @@ constexpr size_t kSmemMax3(size_t a, size_t b, size_t c) { return a > b ? (a > c
 constexpr size_t kChainSmem =
     1024 + kSmemMax3(kOffXq + 2 * kSlotBytes, kSkipBars + 8448, kPairBias + 1024);
 
-// z stash row base of (tile, layer): [tile pair][L][16 pieces][128 rows][16 B]
-__device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int L, int l) {
-  return reinterpret_cast<uint4*>(zimg + ((size_t)(tile >> 1) * L + l) * 2 * kTile) +
+// z stash row base of (tile, ring slot): [tile pair][zring][16 pieces][128 rows][16 B]. The
+// fused kernel keeps a ring of zring (< L) layers per pair -- small enough to stay in L2,
+// where the whole-step stash (42 MB for cfg4) was written back to DRAM; the unfused path's
+// skip GEMM needs all L layers (zring = L, slot = layer).
+__device__ __forceinline__ uint4* zstash_rows(uint8_t* zimg, int tile, int zring, int slot) {
+  return reinterpret_cast<uint4*>(zimg + ((size_t)(tile >> 1) * zring + slot) * 2 * kTile) +
          (tile & 1) * kChainRows;
+}
+__device__ __forceinline__ const uint8_t* zstash_tile(const ChainArgs& a, int p, int g) {
+  return a.zimg + ((size_t)p * a.zring + g % a.zring) * 2 * kTile;
+}
+// A tail producer has its stage of layer g back, so layer g-2's z has been read: count it
+// (the chain waits for it before reusing that ring slot)
+__device__ __forceinline__ void zring_consumed(const ChainArgs& a, int p, int g) {
+  if (a.zfree != nullptr && g >= 2)
+    asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.zfree + p) : "memory");
 }
 
 // ---- skip role: s = ReLU(sum_l W_skip_l z_l + sum_l b_skip_l) for one 128-row tile pair and
@@ -167,12 +179,13 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
         for (int l = 0; l < L; ++l) {
           const int g = i * L + l, st = g & 1;
           mbar_wait(empty + st, ((uint32_t)(g >> 1) & 1) ^ 1);
+          zring_consumed(a, p, g);
           wait_counter(a.zflag + p, 2u * (uint32_t)(g + 1));
           if (l == L - 1) trace_g(a, k == 0, 2);
           fence_proxy_async_all();
           uint8_t* stage = smem + st * kSkipStage;
           mbar_arrive_expect_tx(full + st, 2 * kTile + bbytes);
-          bulk_g2s(stage, a.zimg + ((size_t)p * L + l) * 2 * kTile, 2 * kTile, full + st);
+          bulk_g2s(stage, zstash_tile(a, p, g), 2 * kTile, full + st);
           bulk_g2s(stage + 2 * kTile, a.wskip2 + ((size_t)e * L + l) * bbytes, bbytes, full + st);
         }
         if (heads) tail_loads(false, i);
@@ -411,6 +424,7 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
         for (int l = 0; l < L; ++l) {
           const int g = i * L + l, st = g & 1;
           mbar_wait(empty + st, ((uint32_t)(g >> 1) & 1) ^ 1);
+          zring_consumed(a, p, g);
           // the layer's skip weights do not depend on the chain: in flight before z is --
           // except in layers 0 and 1, whose stages overlap the previous step's s / h image
           // and head weight ring until the chain's z (behind that step's selection) says
@@ -423,7 +437,7 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
           if (l == L - 1) trace_g(a, k == 0, 2);
           if (l < 2) bulk_g2s(stage + 2 * kTile, wsrc, 65536, full + st);
           fence_proxy_async_all();
-          bulk_g2s(stage, a.zimg + ((size_t)p * L + l) * 2 * kTile, 2 * kTile, full + st);
+          bulk_g2s(stage, zstash_tile(a, p, g), 2 * kTile, full + st);
         }
         // the step's last acquire in this SM is behind: the logits bias stays in L1 until
         // the selection reads it
@@ -917,6 +931,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         }
       }
     };
+    uint32_t zseen = 0;  // tail reads of the z ring observed (lane 0)
     load_slot(0);
     if (G > 1) load_slot(1);
     else cp_async_commit();
@@ -924,6 +939,9 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     for (int g = 0; g < G; ++g) {
       const int l = g % L;
       const uint32_t par = (uint32_t)g & 1;
+      // the tail's z-ring read count, loaded now and looked at before the stash below
+      uint32_t zpeek = 0;
+      if (a.zfree != nullptr && lane == 0 && g >= a.zring) zpeek = ld_relaxed_gpu(a.zfree + (tile >> 1));
       // push x_l (P0 xt columns, lanes 0..15) into ring slot (t mod d_l); this thread's pop
       // of its row of that slot completed before store_xd of this layer
       mbar_wait(xt_ready, par);
@@ -941,10 +959,20 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         store_xd(g + 1);
         if (tq) trace_at(a, (g + 1) % L, T_Q_XD, clock64());
       }
-      // z stash of layer l (P1 z columns: lanes 16..31 of the quadrant hold the rows)
+      // z stash of layer g (P1 z columns: lanes 16..31 of the quadrant hold the rows) into
+      // ring slot g % zring, once the tail blocks have read layer g - zring from it (the
+      // count observed last usually covers several layers ahead)
+      if (a.zfree != nullptr && g >= a.zring) {
+        const uint32_t need = (uint32_t)a.ztail * (uint32_t)(g - a.zring + 1);
+        if (lane == 0) {
+          zseen = max(zseen, zpeek);  // the count read at the top of this layer
+          if (zseen < need) zseen = wait_counter_val(a.zfree + (tile >> 1), need);
+        }
+        __syncwarp();
+      }
       mbar_wait(z1_ready, par);
       tc_fence_after();
-      tmem_to_pieces(kColZ, zstash_rows(a.zimg, tile, L, l) + r, 2 * kChainRows, !act);
+      tmem_to_pieces(kColZ, zstash_rows(a.zimg, tile, a.zring, g % a.zring) + r, 2 * kChainRows, !act);
       tc_fence_before();
       mbar_arrive(z_read);
       mbar_arrive(z_stashed);  // warp 14 publishes them (its release fence waits on the stores)

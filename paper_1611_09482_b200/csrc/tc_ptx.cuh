@@ -150,6 +150,12 @@ __device__ __forceinline__ void wait_counter(const uint32_t* p, uint32_t target)
   (void)ld_acquire_gpu(p);
 }
 
+// wait_counter returning the value it observed (>= target)
+__device__ __forceinline__ uint32_t wait_counter_val(const uint32_t* p, uint32_t target) {
+  wait_counter(p, target);
+  return ld_relaxed_gpu(p);
+}
+
 __device__ __forceinline__ long long globaltimer_ns() {
   long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
