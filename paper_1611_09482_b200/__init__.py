@@ -33,11 +33,12 @@ from .fast import (
     push_phase,
 )
 from .generate import CellGenerator, Sampler, cell_fast_generate, init_cell_state
+from .naive import NaiveCellGenerator, cell_naive_generate
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ACTIVATIONS", "CellConfig", "CellGenerator", "CellLayer", "CellModel", "GenerationState",
+    "ACTIVATIONS", "CellConfig", "CellGenerator", "NaiveCellGenerator", "cell_naive_generate", "CellLayer", "CellModel", "GenerationState",
     "LayerWeights", "MacCount", "Model", "ModelConfig", "QueueStateError", "RecurrentInputs",
     "SampleSequence", "Sampler", "build_cell_model", "build_model", "cell_fast_generate",
     "compute_step", "count_macs", "fast_generate", "fast_step", "init_cell_state", "init_state",

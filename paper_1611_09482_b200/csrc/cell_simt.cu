@@ -23,11 +23,13 @@
 namespace fw {
 namespace {
 
-constexpr int NT = 256;
+// threads per CTA: a template parameter, 256 (1024 at one stream per CTA measured slower:
+// the barriers cost more than the extra loads in flight gain)
 
 struct SimtParams {
   CellDims d;
   int B;
+  int pre_pop;  // all layers' pops at the top of each step ([L][BT][R] floats of smem)
   const int* dil;
   const int64_t* qoff;
   float* queue;
@@ -36,7 +38,7 @@ struct SimtParams {
 };
 
 // out[b][o] = epi(b, o, sum_c WT[c][o] * in[b][c]) for o < N, b < BT.
-template <int BT, typename Epi>
+template <int NT, int BT, typename Epi>
 __device__ __forceinline__ void gemv(const float* __restrict__ WT, int K, int N,
                                      const float* in, int ldin, float* red, Epi epi) {
   const int tid = threadIdx.x;
@@ -46,6 +48,19 @@ __device__ __forceinline__ void gemv(const float* __restrict__ WT, int K, int N,
 #pragma unroll
       for (int b = 0; b < BT; ++b) acc[b] = 0.f;
       int c = 0;
+      // 16 independent weight loads in flight per thread: at batch 1 the loop is a chain of
+      // L2 round trips, not FMA-bound (same summation order as the 4-wide loop below)
+      for (; c + 16 <= K; c += 16) {
+        float w[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) w[j] = __ldg(WT + (size_t)(c + j) * N + o);
+#pragma unroll
+        for (int b = 0; b < BT; ++b) {
+          const float* x = in + b * ldin + c;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[b] = fmaf(w[j], x[j], acc[b]);
+        }
+      }
       for (; c + 4 <= K; c += 4) {
         float w0 = __ldg(WT + (size_t)(c + 0) * N + o);
         float w1 = __ldg(WT + (size_t)(c + 1) * N + o);
@@ -79,7 +94,17 @@ __device__ __forceinline__ void gemv(const float* __restrict__ WT, int K, int N,
 #pragma unroll
   for (int b = 0; b < BT; ++b) acc[b] = 0.f;
   if (g < G) {
-    for (int c = k0; c < k1; ++c) {
+    int c = k0;
+    for (; c + 16 <= k1; c += 16) {
+      float w[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) w[j] = __ldg(WT + (size_t)(c + j) * N + o);
+#pragma unroll
+      for (int b = 0; b < BT; ++b)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[b] = fmaf(w[j], in[b * ldin + c + j], acc[b]);
+    }
+    for (; c < k1; ++c) {
       float w0 = __ldg(WT + (size_t)c * N + o);
 #pragma unroll
       for (int b = 0; b < BT; ++b) acc[b] = fmaf(w0, in[b * ldin + c], acc[b]);
@@ -94,6 +119,11 @@ __device__ __forceinline__ void gemv(const float* __restrict__ WT, int K, int N,
     for (int gg = 0; gg < G; ++gg) v += red[(gg * BT + b) * N + oo];
     epi(b, oo, v);
   }
+}
+
+// the pre-pop buffer follows the class ids (16-byte aligned)
+__device__ __forceinline__ float* cls_end(int* cls, int bt) {
+  return reinterpret_cast<float*>(cls + ((bt + 3) & ~3));
 }
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
@@ -159,7 +189,7 @@ __device__ int select_class(const float* lg, int A, int mode, uint32_t prefix) {
   return bi;
 }
 
-template <int BT>
+template <int BT, int NT>
 __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
   extern __shared__ float smem[];
   const CellDims d = p.d;
@@ -181,6 +211,13 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
 
   if (tid < BT) cls[tid] = (tid < nb) ? run.inputs[s0 + tid] : 0;
   __syncthreads();
+  // pops of all layers at the top of the step, when they fit: x_l[t-d] does not depend on
+  // the step's chain, so the ring reads leave the per-layer dependency chain (at small batch
+  // each was an L2/HBM round trip per layer)
+  const bool pre_pop = p.pre_pop != 0;
+  float* xd_all = cls_end(cls, BT);  // [L][BT][R] when pre_pop
+  const int Rp = (R + 3) & ~3;       // channels padded to whole 16-byte chunks
+  const size_t slot_elems = (size_t)((B + 127) / 128) * 128 * Rp;
 
   for (int i = 0; i < run.n_steps; ++i) {
     const int64_t t = run.t0 + i;
@@ -190,6 +227,15 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
       xx[b * 2 * R + r] = __ldg(p.w.embed + (size_t)cls[b] * R + r);
     }
     for (int e = tid; e < BT * S; e += NT) s[e] = 0.f;
+    if (pre_pop) {
+      for (int e = tid; e < L * nb * R; e += NT) {
+        const int l = e / (nb * R), rest = e % (nb * R);
+        const int b = rest / R, r = rest % R;
+        const int st = s0 + b;
+        const float* q = p.queue + p.qoff[l] + (size_t)(t % p.dil[l]) * slot_elems;
+        xd_all[(l * BT + b) * R + r] = q[((size_t)((st >> 7) * (Rp / 4) + (r >> 2)) * 128 + (st & 127)) * 4 + (r & 3)];
+      }
+    }
     __syncthreads();
 
     for (int l = 0; l < L; ++l) {
@@ -198,8 +244,6 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
       // (stream s, channel r) at ((s/128 * R/4 + r/4) * 128 + s%128) * 4 + r%4; e walks the
       // tile's streams contiguously per 16-byte channel chunk.
       const int dl = p.dil[l];
-      const int Rp = (R + 3) & ~3;  // channels padded to whole 16-byte chunks
-      const size_t slot_elems = (size_t)((B + 127) / 128) * 128 * Rp;
       float* q = p.queue + p.qoff[l] + (size_t)(t % dl) * slot_elems;
       for (int e = tid; e < nb * Rp; e += NT) {
         const int j = e & 3, rest = e >> 2;
@@ -208,13 +252,13 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
         if (r >= R) continue;
         const int s = s0 + b;
         float* slot = q + ((size_t)((s >> 7) * (Rp / 4) + c4) * 128 + (s & 127)) * 4 + j;
-        const float old = *slot;
+        const float old = pre_pop ? xd_all[(l * BT + b) * R + r] : *slot;
         *slot = xx[b * 2 * R + r];
         xx[b * 2 * R + R + r] = old;
       }
       __syncthreads();
       const float* db = p.w.dil_b + (size_t)l * 2 * D;
-      gemv<BT>(p.w.dilT + (size_t)l * 2 * R * 2 * D, 2 * R, 2 * D, xx, 2 * R, red,
+      gemv<NT, BT>(p.w.dilT + (size_t)l * 2 * R * 2 * D, 2 * R, 2 * D, xx, 2 * R, red,
                [&](int b, int o, float v) { a[b * 2 * D + o] = v + db[o]; });
       __syncthreads();
       for (int e = tid; e < BT * D; e += NT) {
@@ -223,12 +267,12 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
       }
       __syncthreads();
       const float* sb = p.w.skip_b + (size_t)l * S;
-      gemv<BT>(p.w.skipT + (size_t)l * D * S, D, S, z, D, red,
+      gemv<NT, BT>(p.w.skipT + (size_t)l * D * S, D, S, z, D, red,
                [&](int b, int o, float v) { s[b * S + o] += v + sb[o]; });
       if (l + 1 < L) {
         __syncthreads();
         const float* rb = p.w.res_b + (size_t)l * R;
-        gemv<BT>(p.w.resT + (size_t)l * D * R, D, R, z, D, red,
+        gemv<NT, BT>(p.w.resT + (size_t)l * D * R, D, R, z, D, red,
                  [&](int b, int o, float v) { xx[b * 2 * R + o] += v + rb[o]; });
       }
       __syncthreads();
@@ -236,10 +280,10 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
     // head: logits = W2 relu(W1 relu(s) + b1) + b2
     for (int e = tid; e < BT * S; e += NT) s[e] = fmaxf(s[e], 0.f);
     __syncthreads();
-    gemv<BT>(p.w.h1T, S, H, s, S, red,
+    gemv<NT, BT>(p.w.h1T, S, H, s, S, red,
              [&](int b, int o, float v) { hb[b * H + o] = fmaxf(v + p.w.h1_b[o], 0.f); });
     __syncthreads();
-    gemv<BT>(p.w.h2T, H, A, hb, H, red,
+    gemv<NT, BT>(p.w.h2T, H, A, hb, H, red,
              [&](int b, int o, float v) { lg[b * A + o] = v + p.w.h2_b[o]; });
     __syncthreads();
 
@@ -261,20 +305,29 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
   }
 }
 
-template <int BT>
-size_t smem_bytes(const CellDims& d) {
-  return sizeof(float) * (size_t)(BT * (2 * d.R + 2 * d.D + d.D + d.S + d.H + d.A) + NT * BT) +
-         sizeof(int) * BT;
-}
+constexpr size_t kPrePopMax = 64 * 1024;  // bytes of smem the pre-pop buffer may take
 
 template <int BT>
+size_t pre_pop_bytes(const CellDims& d) {
+  return sizeof(float) * (size_t)d.L * BT * d.R;
+}
+template <int BT, int NT>
+size_t smem_bytes(const CellDims& d) {
+  const size_t pp = pre_pop_bytes<BT>(d);
+  return sizeof(float) * (size_t)(BT * (2 * d.R + 2 * d.D + d.D + d.S + d.H + d.A) + NT * BT) +
+         sizeof(int) * ((BT + 3) & ~3) + (pp <= kPrePopMax ? pp : 0);
+}
+
+template <int BT, int NT = 256>
 cudaError_t launch_bt(const SimtParams& p, cudaStream_t st) {
-  const size_t sm = smem_bytes<BT>(p.d);
-  cudaError_t e = cudaFuncSetAttribute(cell_simt_kernel<BT>,
+  const size_t sm = smem_bytes<BT, NT>(p.d);
+  SimtParams q = p;
+  q.pre_pop = pre_pop_bytes<BT>(p.d) <= kPrePopMax ? 1 : 0;
+  cudaError_t e = cudaFuncSetAttribute(cell_simt_kernel<BT, NT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   const int grid = (p.B + BT - 1) / BT;
-  cell_simt_kernel<BT><<<grid, NT, sm, st>>>(p);
+  cell_simt_kernel<BT, NT><<<grid, NT, sm, st>>>(q);
   return cudaGetLastError();
 }
 

@@ -163,3 +163,34 @@ def test_fast_generate_long_primer_uses_prefill(cuda, models):
     top = np.sort(lg)[-2:]
     if top[1] - top[0] > 1e-3:
         assert a[0, 0] == b[0, 0] == int(np.argmax(lg))
+
+
+# ---- naive (cache-free) generation on the GPU -----------------------
+
+def test_naive_logits_match_oracle_demand_plan(cuda, models):
+    """Each naive step's logits against the oracle's demand-driven naive_logits (the
+    reference's naive.py plan), inside and beyond the receptive field."""
+    from paper_1611_09482_b200 import NaiveCellGenerator
+
+    model = models["simt"]
+    rf = model.config.receptive_field()
+    hist = teacher(rf + 40, 1, 31)
+    g = NaiveCellGenerator(model, 1, kernel="simt")
+    o = oc.CellOracle(model)
+    h = torch.as_tensor(hist, device="cuda")
+    for n in (1, 2, 17, rf - 1, rf, rf + 1, rf + 40):
+        lg = g.logits(h[:n]).cpu().numpy()[0]
+        ref = o.naive_logits(hist[:n, 0])
+        assert np.max(np.abs(lg - ref)) <= 1e-4, n
+
+
+def test_naive_generation_equals_fast(cuda, models):
+    """Greedy generation: naive (recompute per step) and fast (queues) agree."""
+    from paper_1611_09482_b200 import cell_fast_generate, cell_naive_generate
+
+    model = models["simt"]
+    primer = [5, 17, 128]
+    a = cell_naive_generate(model, primer, 60, kernel="simt")
+    b = cell_fast_generate(model, primer, 60, kernel="simt")
+    assert a.shape == b.shape == (1, 60)
+    assert np.array_equal(a, b)
