@@ -237,3 +237,19 @@ def test_invalid_arguments(cuda, cfg1_model):
     with pytest.raises(ValueError):
         cell_fast_generate(cfg1_model, [300], 4)
     assert cell_fast_generate(cfg1_model, [1], 0).shape == (1, 0)
+
+
+@pytest.mark.parametrize("cluster", ["0", "2", "4", "8"])
+def test_small_batch_cluster_kernel_matches_oracle(cuda, cfg1_model, monkeypatch, cluster):
+    """The cluster-per-stream SIMT kernel (FW_SIMT_CLUSTER) and the per-CTA kernel give the
+    oracle's teacher-forced logits on the same inputs, for 1 and 3 streams."""
+    monkeypatch.setenv("FW_SIMT_CLUSTER", cluster)
+    for B in (1, 3):
+        cls = np.random.default_rng(40 + B).integers(0, 256, (60, B))
+        gen = CellGenerator(cfg1_model, B, kernel="simt")
+        out, lg = run(gen, cls, 60, Sampler(0), 60)
+        o = oc.CellOracle(cfg1_model)
+        for b in range(B):
+            ref = o.forward_full(cls[:, b])
+            assert np.max(np.abs(lg[:, b] - ref)) <= 1e-4, (cluster, B, b)
+            assert np.array_equal(out[:, b], np.argmax(lg[:, b], axis=1))
