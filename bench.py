@@ -283,7 +283,9 @@ def main():
     gen.reset()
     host_in = torch.full((1, B), spec.primer_class, dtype=torch.int32).pin_memory().numpy()
     host_out = torch.empty((args.steps, B), dtype=torch.int32).pin_memory().numpy()
-    gen.generate_host(host_in, 1, sampler, out=host_out[:1])  # warm the host path
+    # warm the host path at the timed size (the library's device staging buffer grows to
+    # the largest call it has seen; a first call at a new size allocates)
+    gen.generate_host(host_in, args.steps, sampler, out=host_out)
     gen.reset()
     barrier()
     torch.cuda.synchronize()
