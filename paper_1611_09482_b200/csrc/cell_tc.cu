@@ -644,6 +644,9 @@ bool tc_supported(const CellDims& d, int batch, std::string* why) {
   if (d.S % 128 || d.H % 128 || d.S > 2048 || d.H > 2048) return no("needs skip/head multiples of 128");
   if (d.A != 256) return no("needs 256 classes");
   if (d.L > kMaxChainLayers) return no("needs at most 128 layers");
+  // the chain's pops are staged two layers ahead of their use; with fewer than 3 layers that
+  // is the same layer of the next step, read before this step's push of it
+  if (d.L < 3) return no("needs at least 3 layers");
   if (batch % 128) return no("needs a batch that is a multiple of 128 streams");
   return true;
 }

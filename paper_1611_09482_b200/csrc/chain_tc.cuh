@@ -877,7 +877,8 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     // pops: each thread copies its own row of layer g's slot into staging buffer Xq[g & 1]
     // (16 x 16 B, cp.async) two layers ahead -- no registers held across layers, and the
     // same thread wrote that row with its push, so plain program order covers the reuse of
-    // ring slots within a launch. K-piece j (K 8j..8j+7) of row r is the 16 bytes at
+    // ring slots within a launch (the copy of layer g+2 is issued before the push of layer
+    // g: with L >= 3, tc_supported, those are different layers). K-piece j (K 8j..8j+7) of row r is the 16 bytes at
     // (j * 64 + r) * 16: packed words 4j .. 4j+3 of the operand row.
     uint8_t* xq = smem + kOffXq;
     auto load_slot = [&](int g) {

@@ -253,3 +253,20 @@ def test_small_batch_cluster_kernel_matches_oracle(cuda, cfg1_model, monkeypatch
             ref = o.forward_full(cls[:, b])
             assert np.max(np.abs(lg[:, b] - ref)) <= 1e-4, (cluster, B, b)
             assert np.array_equal(out[:, b], np.argmax(lg[:, b], axis=1))
+
+
+def test_tcgen05_needs_three_layers_and_short_stacks_fall_back(cuda):
+    """bf16 stacks of 1-2 layers are outside the tcgen05 kernel (its pops are staged two
+    layers ahead); auto selection serves them with the SIMT kernel, at parity."""
+    for L in (1, 2):
+        m = build_cell_model(CellConfig(1, L, 128, 128, 256, weight_dtype="bf16", bias="fan_in",
+                                        init_seed=5))
+        with pytest.raises(ValueError):
+            CellGenerator(m, 128, kernel="tcgen05")
+        gen = CellGenerator(m, 128)
+        assert gen.kernel == "simt"
+        cls = np.random.default_rng(L).integers(0, 256, (6, 128))
+        _, lg = run(gen, cls, 6, Sampler(0), 6)
+        o = oc.CellOracle(m, exact=False)
+        for b in (0, 127):
+            assert np.max(np.abs(lg[:, b] - o.forward_full(cls[:, b]))) <= 2e-2
