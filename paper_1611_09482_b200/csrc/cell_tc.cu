@@ -877,7 +877,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
     // as soon as the pair's selection of step i is written (counters, no host round trip)
     const int timed = h.timing ? timing_reserve(h, 1) : 0;
     if (timed) cudaEventRecord(h.tev[0], st);
-    static const int per_launch = getenv("FW_STEPS_PER_LAUNCH") ? atoi(getenv("FW_STEPS_PER_LAUNCH")) : 0;
+    const int per_launch = getenv("FW_STEPS_PER_LAUNCH") ? atoi(getenv("FW_STEPS_PER_LAUNCH")) : 0;
     const int chunk = per_launch > 0 ? per_launch : run.n_steps;
     for (int i0 = 0; i0 < run.n_steps; i0 += chunk) {
       ca.n_steps = std::min(chunk, run.n_steps - i0);

@@ -270,3 +270,28 @@ def test_tcgen05_needs_three_layers_and_short_stacks_fall_back(cuda):
         o = oc.CellOracle(m, exact=False)
         for b in (0, 127):
             assert np.max(np.abs(lg[:, b] - o.forward_full(cls[:, b]))) <= 2e-2
+
+
+TC_GRID = [(L, S, H, B) for L in (3, 5, 12) for (S, H) in ((128, 128), (256, 256), (512, 256),
+                                                           (512, 512), (1024, 512))
+           for B in (128, 384)]
+
+
+@pytest.mark.parametrize("L,S,H,B", TC_GRID)
+def test_tcgen05_shape_grid_teacher_forced(cuda, monkeypatch, L, S, H, B):
+    """The tcgen05 kernel over its shape space (fused pair tail, fused global tail, per-step
+    path; one and several tile pairs; several steps per launch and one), teacher-forced
+    logits against the oracle within the bf16 tolerance on the first, a middle and the last
+    stream."""
+    m = build_cell_model(CellConfig(1, L, 128, 128, S, head_channels=H, weight_dtype="bf16",
+                                    bias="fan_in", init_seed=L + S + H))
+    o = oc.CellOracle(m, exact=False)
+    cls = np.random.default_rng(B + L).integers(0, 256, (5, B))
+    for per_launch in ("0", "2"):
+        monkeypatch.setenv("FW_STEPS_PER_LAUNCH", per_launch)
+        gen = CellGenerator(m, B, kernel="tcgen05")
+        _, lg = run(gen, cls, 5, Sampler(0), 5)
+        for b in (0, B // 2 + 1, B - 1):
+            dev = np.max(np.abs(lg[:, b] - o.forward_full(cls[:, b])))
+            assert dev <= 2e-2, (per_launch, b, dev)
+        gen.close()
