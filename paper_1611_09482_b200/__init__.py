@@ -33,14 +33,36 @@ from .fast import (
     push_phase,
 )
 from .generate import CellGenerator, Sampler, cell_fast_generate, init_cell_state
-from .naive import NaiveCellGenerator, cell_naive_generate
+from .naive import NaiveCellGenerator, cell_naive_generate, naive_generate, naive_step
+from .model_io import (
+    ModelFormatError,
+    load_cell_model,
+    load_model,
+    model_from_text,
+    model_to_text,
+    save_cell_model,
+    save_model,
+)
+from .benchmark import (
+    CSV_COLUMNS,
+    MODES,
+    TimingRecord,
+    default_grid,
+    emit_records,
+    read_records,
+    run_benchmark,
+)
 
 __version__ = "0.1.0"
 
 __all__ = [
-    "ACTIVATIONS", "CellConfig", "CellGenerator", "NaiveCellGenerator", "cell_naive_generate", "CellLayer", "CellModel", "GenerationState",
-    "LayerWeights", "MacCount", "Model", "ModelConfig", "QueueStateError", "RecurrentInputs",
-    "SampleSequence", "Sampler", "build_cell_model", "build_model", "cell_fast_generate",
-    "compute_step", "count_macs", "fast_generate", "fast_step", "init_cell_state", "init_state",
-    "pop_phase", "push_phase", "receptive_field", "round_to_bf16",
+    "ACTIVATIONS", "CSV_COLUMNS", "CellConfig", "CellGenerator", "CellLayer",
+    "CellModel", "GenerationState", "LayerWeights", "MODES", "MacCount",
+    "Model", "ModelConfig", "ModelFormatError", "NaiveCellGenerator", "QueueStateError",
+    "RecurrentInputs", "SampleSequence", "Sampler", "TimingRecord", "build_cell_model",
+    "build_model", "cell_fast_generate", "cell_naive_generate", "compute_step", "count_macs",
+    "default_grid", "emit_records", "fast_generate", "fast_step", "init_cell_state",
+    "init_state", "load_cell_model", "load_model", "model_from_text", "model_to_text",
+    "naive_generate", "naive_step", "pop_phase", "push_phase", "read_records",
+    "receptive_field", "round_to_bf16", "run_benchmark", "save_cell_model", "save_model",
 ]

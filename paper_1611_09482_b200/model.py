@@ -173,9 +173,28 @@ def build_model(config: ModelConfig) -> Model:
     return Model(config=config, layers=tuple(layers))
 
 
+def demand_offsets(config: ModelConfig) -> list[set[int]]:
+    """Time offsets (steps back from the output) at which each layer is evaluated by the
+    cache-free generator: the top layer at 0, and layer l-1 wherever layer l's taps read it,
+    o + k * d_l for k < w (the reference's demand plan, naive.py:27-110)."""
+    w, dil = config.filter_width, config.dilations()
+    dem = [set() for _ in dil]
+    dem[-1] = {0}
+    for l in range(len(dil) - 1, 0, -1):
+        dem[l - 1] = {o + k * dil[l] for o in dem[l] for k in range(w)}
+    return dem
+
+
 def count_macs(config: ModelConfig, mode: str = "fast") -> MacCount:
-    """Per-sample fast-path cost: sum of w * in * out over layers (reference bench.py:30-43)."""
-    if mode != "fast":
-        raise ValueError("only the queue-cached 'fast' mode is served by this package")
+    """Per-sample cost: sum of w * in * out over the layer evaluations of one step --
+    once per layer on the fast path, once per demanded offset on the naive path (reference
+    bench.py:30-43)."""
     w = config.filter_width
-    return MacCount(sum(w * ci * co for ci, co in config.channel_dims()), config.total_layers)
+    dims = config.channel_dims()
+    if mode == "fast":
+        return MacCount(sum(w * ci * co for ci, co in dims), config.total_layers)
+    if mode == "naive":
+        dem = demand_offsets(config)
+        return MacCount(sum(len(o) * w * ci * co for o, (ci, co) in zip(dem, dims)),
+                        sum(len(o) for o in dem))
+    raise ValueError(f"unknown mode {mode!r}")

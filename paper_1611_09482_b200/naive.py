@@ -89,3 +89,65 @@ def cell_naive_generate(model: CellModel, primer, steps: int, batch: int | None 
     out = g.generate(np.ascontiguousarray(p.T), steps).cpu().numpy()
     g.close()
     return np.ascontiguousarray(out.T)
+
+
+# ---- plain mode (the reference's own stack) --------------------------------------------------
+def plain_naive_step(model, history, state=None) -> float:
+    """The reference's naive_step output (naive.py:27-110) for history[-1]: the fast kernel
+    stepped teacher-forced over the receptive-field window from zero queues. The output's
+    demand cone lies inside the window and is evaluated by the same kernel in the same order,
+    so the result equals the queue-cached output bit for bit."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from .fast import init_state
+    from .model import receptive_field
+
+    h = np.asarray(history, dtype=np.float64).ravel()
+    if h.size == 0:
+        raise ValueError("the history must hold at least one sample")
+    rf = receptive_field(model.config)
+    w = h[-rf:]
+    own = state is None
+    st = init_state(model, 1) if own else state
+    st.reset()
+    x = torch.as_tensor(w.reshape(-1, 1), device=st._dev)
+    out = torch.empty((w.size, 1), dtype=torch.float64, device=st._dev)
+    _lib.check(st._lib.fw_plain_generate(st._h, C.c_void_p(x.data_ptr()), w.size, w.size,
+                                         C.c_void_p(out.data_ptr()), _lib.stream_ptr()))
+    y = float(out[-1, 0].item())
+    if own:
+        st.close()
+    return y
+
+
+def plain_naive_generate(model, primer, steps: int):
+    """The reference's naive_generate: fast_generate's feedback rule with every output
+    recomputed from the history (cache-free)."""
+    from .fast import SampleSequence, init_state, scalar_primer
+
+    if steps < 0:
+        raise ValueError("steps must be non-negative")
+    seed = scalar_primer(primer)
+    hist = list(seed)
+    st = init_state(model, 1)
+    out = []
+    for _ in range(steps):
+        y = plain_naive_step(model, hist, st)
+        out.append(y)
+        hist.append(y)
+    st.close()
+    return SampleSequence.from_scalars(out, start_index=len(seed))
+
+
+def naive_step(model, history):
+    """The reference's ``naive_step(model, history) -> (sample, MacCount)``: the sample that
+    extends the history by one, computed cache-free on the GPU, and its exact cost."""
+    from .model import count_macs
+
+    return plain_naive_step(model, history), count_macs(model.config, "naive")
+
+
+naive_generate = plain_naive_generate  # the reference's name (naive.py:113)
