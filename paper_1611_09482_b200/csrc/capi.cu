@@ -73,6 +73,10 @@ void free_cell(Handle& h) {
   h.d_qoff = nullptr;
   if (h.tc) tc_destroy(h);
   prefill_destroy(h);
+  if (h.d_pad) cudaFree(h.d_pad);
+  if (h.d_pad_lg) cudaFree(h.d_pad_lg);
+  h.d_pad = nullptr;
+  h.d_pad_lg = nullptr;
 }
 
 void free_plain(Handle& h) {
@@ -118,7 +122,48 @@ int validate_sampler(const fw_sampler* s) {
   return FW_OK;
 }
 
+int run_cell_dev(Handle& h, const CellRun& run, cudaStream_t st);
+
+template <typename T>
+int grow(T** p, int64_t* have, int64_t need) {
+  if (need <= *have) return FW_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *have = 0;
+  FW_CUDA(cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * (size_t)need));
+  *have = need;
+  return FW_OK;
+}
+
+// The caller's buffers hold user_batch streams per step; a padded handle (tcgen05 with a
+// batch that is not a multiple of 128) runs batch >= user_batch streams on the device, the
+// extra ones fed class 0 and discarded. Stage inputs, outputs and logits through [n][batch]
+// buffers with strided copies.
 int run_cell(Handle& h, const CellRun& run, cudaStream_t st) {
+  if (h.user_batch == h.batch) return run_cell_dev(h, run, st);
+  const int64_t B = h.user_batch, Bp = h.batch, A = h.dims.A;
+  if (int rc = grow(&h.d_pad, &h.d_pad_elems, ((int64_t)run.n_inputs + run.n_steps) * Bp)) return rc;
+  if (run.logits && run.n_logit_steps)
+    if (int rc = grow(&h.d_pad_lg, &h.d_pad_lg_elems, (int64_t)run.n_logit_steps * Bp * A)) return rc;
+  int32_t* in = h.d_pad;
+  int32_t* out = h.d_pad + (int64_t)run.n_inputs * Bp;
+  FW_CUDA(cudaMemsetAsync(in, 0, sizeof(int32_t) * (size_t)run.n_inputs * Bp, st));
+  FW_CUDA(cudaMemcpy2DAsync(in, sizeof(int32_t) * Bp, run.inputs, sizeof(int32_t) * B,
+                            sizeof(int32_t) * B, run.n_inputs, cudaMemcpyDeviceToDevice, st));
+  CellRun r = run;
+  r.inputs = in;
+  r.out = out;
+  r.logits = (run.logits && run.n_logit_steps) ? h.d_pad_lg : nullptr;
+  if (int rc = run_cell_dev(h, r, st)) return rc;
+  FW_CUDA(cudaMemcpy2DAsync(run.out, sizeof(int32_t) * B, out, sizeof(int32_t) * Bp,
+                            sizeof(int32_t) * B, run.n_steps, cudaMemcpyDeviceToDevice, st));
+  if (r.logits)
+    FW_CUDA(cudaMemcpy2DAsync(run.logits, sizeof(float) * B * A, h.d_pad_lg, sizeof(float) * Bp * A,
+                              sizeof(float) * B * A, run.n_logit_steps, cudaMemcpyDeviceToDevice, st));
+  return FW_OK;
+}
+
+int run_cell_dev(Handle& h, const CellRun& run, cudaStream_t st) {
   cudaError_t e;
   int64_t launches = 0;
   if (h.kernel == FW_KERNEL_TCGEN05) {
@@ -171,13 +216,16 @@ int fw_cell_create(const fw_cell_desc* desc, int32_t batch, int32_t device, int3
   Handle& h = fh->h;
   h.device = device;
   h.batch = batch;
+  h.user_batch = batch;
   const int L = desc->n_layers, R = desc->residual_channels, D = desc->dilation_channels;
   const int S = desc->skip_channels, H = desc->head_channels, A = desc->classes;
   h.dims = CellDims{L, R, D, S, H, A, desc->weight_dtype};
   h.dil.assign(desc->dilations, desc->dilations + L);
 
+  // tcgen05 tiles hold 128 streams: other batches of >= 128 run padded to the next multiple
+  const int padded = batch >= 128 ? (batch + 127) / 128 * 128 : batch;
   std::string why;
-  const bool tc_ok = tc_supported(h.dims, batch, &why);
+  const bool tc_ok = tc_supported(h.dims, padded, &why);
   if (kernel == FW_KERNEL_TCGEN05 && !tc_ok) {
     delete fh;
     return invalid("tcgen05 kernel unsupported for this shape: " + why);
@@ -185,6 +233,7 @@ int fw_cell_create(const fw_cell_desc* desc, int32_t batch, int32_t device, int3
   h.kernel = (kernel == FW_KERNEL_TCGEN05 || (kernel == FW_KERNEL_AUTO && tc_ok))
                  ? FW_KERNEL_TCGEN05
                  : FW_KERNEL_SIMT;
+  if (h.kernel == FW_KERNEL_TCGEN05) h.batch = padded;
 
   auto fail = [&](int code) {
     free_cell(h);
@@ -301,7 +350,7 @@ int fw_cell_generate_host(fw_handle* fh, const int32_t* h_inputs, int32_t n_inpu
   Handle& h = fh->h;
   FW_CUDA(cudaSetDevice(h.device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const int64_t need = ((int64_t)n_inputs + n_steps) * h.batch;
+  const int64_t need = ((int64_t)n_inputs + n_steps) * h.user_batch;
   if (need > h.d_io_elems) {
     if (h.d_io) cudaFree(h.d_io);
     h.d_io = nullptr;
@@ -310,13 +359,13 @@ int fw_cell_generate_host(fw_handle* fh, const int32_t* h_inputs, int32_t n_inpu
     h.d_io_elems = need;
   }
   int32_t* d_in = h.d_io;
-  int32_t* d_out = h.d_io + (int64_t)n_inputs * h.batch;
-  FW_CUDA(cudaMemcpyAsync(d_in, h_inputs, sizeof(int32_t) * (size_t)n_inputs * h.batch,
+  int32_t* d_out = h.d_io + (int64_t)n_inputs * h.user_batch;
+  FW_CUDA(cudaMemcpyAsync(d_in, h_inputs, sizeof(int32_t) * (size_t)n_inputs * h.user_batch,
                           cudaMemcpyHostToDevice, st));
   CellRun run{d_in, n_inputs, n_steps, d_out, nullptr, 0, h.t,
               sampler->mode, sampler->seed, sampler->stream_offset};
   if ((rc = run_cell(h, run, st))) return rc;
-  FW_CUDA(cudaMemcpyAsync(h_out, d_out, sizeof(int32_t) * (size_t)n_steps * h.batch,
+  FW_CUDA(cudaMemcpyAsync(h_out, d_out, sizeof(int32_t) * (size_t)n_steps * h.user_batch,
                           cudaMemcpyDeviceToHost, st));
   FW_CUDA(cudaStreamSynchronize(st));
   return FW_OK;
@@ -341,8 +390,23 @@ int fw_cell_prefill(fw_handle* fh, const int32_t* d_inputs, int32_t T, float* d_
   const char* mode = getenv("FW_PREFILL_MODE");
   bool steps = h.kernel == FW_KERNEL_TCGEN05 && h.batch >= 2048;
   if (mode) steps = std::string(mode) == "steps";
-  if (!steps) return cell_prefill(h, d_inputs, T, d_logits, st);
-  const int64_t need = (int64_t)T * h.batch;
+  if (!steps && h.user_batch == h.batch) return cell_prefill(h, d_inputs, T, d_logits, st);
+  if (!steps) {
+    // padded handle: inputs to [T][batch] (pad streams class 0), logits back to [T][user]
+    const int64_t B = h.user_batch, Bp = h.batch, A = h.dims.A;
+    if (int rc2 = grow(&h.d_pad, &h.d_pad_elems, (int64_t)T * Bp)) return rc2;
+    if (d_logits)
+      if (int rc2 = grow(&h.d_pad_lg, &h.d_pad_lg_elems, (int64_t)T * Bp * A)) return rc2;
+    FW_CUDA(cudaMemsetAsync(h.d_pad, 0, sizeof(int32_t) * (size_t)T * Bp, st));
+    FW_CUDA(cudaMemcpy2DAsync(h.d_pad, sizeof(int32_t) * Bp, d_inputs, sizeof(int32_t) * B,
+                              sizeof(int32_t) * B, T, cudaMemcpyDeviceToDevice, st));
+    if (int rc2 = cell_prefill(h, h.d_pad, T, d_logits ? h.d_pad_lg : nullptr, st)) return rc2;
+    if (d_logits)
+      FW_CUDA(cudaMemcpy2DAsync(d_logits, sizeof(float) * B * A, h.d_pad_lg, sizeof(float) * Bp * A,
+                                sizeof(float) * B * A, T, cudaMemcpyDeviceToDevice, st));
+    return FW_OK;
+  }
+  const int64_t need = (int64_t)T * h.user_batch;
   if (need > h.d_io_elems) {
     if (h.d_io) cudaFree(h.d_io);
     h.d_io = nullptr;

@@ -122,7 +122,8 @@ struct Handle {
   int is_plain = 0;
   int device = 0;
   int kernel = FW_KERNEL_SIMT;
-  int32_t batch = 0;
+  int32_t batch = 0;       // streams on the device (tcgen05: padded to a multiple of 128)
+  int32_t user_batch = 0;  // streams in the caller's buffers
   int64_t t = 0;
   int64_t last_launches = 0;
   int popped = 0;
@@ -145,6 +146,11 @@ struct Handle {
   // scratch for the *_host entry points
   int32_t* d_io = nullptr;
   int64_t d_io_elems = 0;
+  // staging between the caller's [n][user_batch] and the device's [n][batch] layouts
+  int32_t* d_pad = nullptr;
+  int64_t d_pad_elems = 0;
+  float* d_pad_lg = nullptr;
+  int64_t d_pad_lg_elems = 0;
 
   // optional per-step kernel timing (fw_debug_timing): events [3i] before the chain
   // kernel of step i, [3i+1] after it, [3i+2] after the step's last kernel

@@ -295,3 +295,27 @@ def test_tcgen05_shape_grid_teacher_forced(cuda, monkeypatch, L, S, H, B):
             dev = np.max(np.abs(lg[:, b] - o.forward_full(cls[:, b])))
             assert dev <= 2e-2, (per_launch, b, dev)
         gen.close()
+
+
+@pytest.mark.parametrize("B", [200, 129])
+def test_tcgen05_padded_batch(cuda, B):
+    """Batches that are not a multiple of 128 run on the tcgen05 kernel padded to the next
+    multiple (extra streams fed class 0, discarded): teacher-forced logits at parity, the
+    host-buffer entry point and the full-sequence forward agree with the device loop."""
+    m = build_cell_model(CellConfig(1, 4, 128, 128, 256, weight_dtype="bf16", bias="fan_in",
+                                    init_seed=9))
+    gen = CellGenerator(m, B)
+    assert gen.kernel == "tcgen05"
+    cls = np.random.default_rng(B).integers(0, 256, (6, B))
+    out, lg = run(gen, cls, 6, Sampler(2, 5), 6)
+    o = oc.CellOracle(m, exact=False)
+    for b in (0, B // 2, B - 1):
+        assert np.max(np.abs(lg[:, b] - o.forward_full(cls[:, b]))) <= 2e-2
+    gen.reset()
+    host = gen.generate_host(cls.astype(np.int32), 6, Sampler(2, 5))
+    assert np.array_equal(host, out)
+    gen.reset()
+    pf = gen.prefill(torch.as_tensor(cls, dtype=torch.int32, device="cuda"), want_logits=True)
+    assert pf.shape == (6, B, 256)
+    assert np.max(np.abs(pf.cpu().numpy() - lg)) <= 2e-2
+    assert gen.step_index == 6
