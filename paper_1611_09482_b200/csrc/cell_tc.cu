@@ -81,7 +81,6 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 320;  // warp 0 producer, warp 1 MMA, warps 2..9 epilogue
 constexpr uint32_t kChunk = 16384;  // one [128 rows][64] bf16 operand image
 constexpr int kChunksPerLayer = 10;  // 8 dil (2 N-halves x 4 K-chunks) + 2 res
 constexpr uint32_t kLayerBytes = kChunksPerLayer * kChunk;
@@ -191,43 +190,6 @@ __device__ __forceinline__ int64_t qbase_of(const ChainArgs& a, int i, int l) {
   return a.qoff[l] + (int64_t)s * a.slot_stride;
 }
 
-__device__ __forceinline__ void ld64(float (&v)[64], const float* p) {
-  const float4* q = reinterpret_cast<const float4*>(p);
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    float4 f = q[i];
-    v[4 * i] = f.x;
-    v[4 * i + 1] = f.y;
-    v[4 * i + 2] = f.z;
-    v[4 * i + 3] = f.w;
-  }
-}
-// 16 float4 chunks at a stride of `stride` floats (queue layout [R/4][B][4]).
-__device__ __forceinline__ void ld64s(float (&v)[64], const float* p, size_t stride) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    float4 f = *reinterpret_cast<const float4*>(p + i * stride);
-    v[4 * i] = f.x;
-    v[4 * i + 1] = f.y;
-    v[4 * i + 2] = f.z;
-    v[4 * i + 3] = f.w;
-  }
-}
-__device__ __forceinline__ void st64s(float* p, const float (&v)[64], size_t stride) {
-#pragma unroll
-  for (int i = 0; i < 16; ++i)
-    *reinterpret_cast<float4*>(p + i * stride) =
-        make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-}
-// 64 fp32 -> one 128-byte bf16 row of a swizzled [128][64] image
-__device__ __forceinline__ void row_to_image(uint32_t img_saddr, int r, const float (&v)[64]) {
-#pragma unroll
-  for (int p = 0; p < 8; ++p)
-    st_shared_v4(img_saddr + swz(r, p), pack_h2(v[8 * p], v[8 * p + 1]),
-                 pack_h2(v[8 * p + 2], v[8 * p + 3]), pack_h2(v[8 * p + 4], v[8 * p + 5]),
-                 pack_h2(v[8 * p + 6], v[8 * p + 7]));
-}
-
 // Gumbel noise -log(-log u) of class cls; v + gumbel_noise(...) == v - log(-log u) exactly.
 __device__ __forceinline__ float gumbel_noise(uint32_t prefix, int cls) {
   const float u = noise_uniform(prefix, (uint32_t)cls);
@@ -235,9 +197,9 @@ __device__ __forceinline__ float gumbel_noise(uint32_t prefix, int cls) {
 }
 
 // ReLU(v + bias[0..32)) -> 16 packed fp16 pairs (bias null: none). The bias (identical for
-// every thread; global
-// or shared memory, hence generic loads) comes in as 8 independent 16-byte loads: scalar
-// loads next to 64 live accumulator values were serialised by the register budget (~2 us
+// every thread; global or shared memory, hence generic loads) comes in as 8 independent
+// 16-byte loads: scalar loads next to 64 live accumulator values were serialised by the
+// register budget (~2 us
 // per 128-column epilogue).
 __device__ __forceinline__ void relu_pack32(const float (&v)[32], const float* bias, uint32_t (&w)[16]) {
   const float4* b4 = reinterpret_cast<const float4*>(bias);
