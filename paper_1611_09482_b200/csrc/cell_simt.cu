@@ -44,7 +44,7 @@ template <int NT, int BT, typename Epi>
 __device__ __forceinline__ void gemv(const float* __restrict__ WT, int K, int N,
                                      const float* in, int ldin, float* red, Epi epi) {
   const int tid = threadIdx.x;
-  if (N >= NT / 2) {
+  if (N >= NT) {
     for (int o = tid; o < N; o += NT) {
       float acc[BT];
 #pragma unroll
@@ -637,6 +637,15 @@ cudaError_t launch_cell_simt(const Handle& h, const CellRun& run, cudaStream_t s
       case 8: return launch_cluster<8>(p, st);
       case 4: return launch_cluster<4>(p, st);
       case 2: return launch_cluster<2>(p, st);
+      default: break;
+    }
+  }
+  if (const char* e = getenv("FW_SIMT_BT")) {  // streams per CTA override (measurements)
+    switch (atoi(e)) {
+      case 8: return launch_bt<8>(p, st);
+      case 4: return launch_bt<4>(p, st);
+      case 2: return launch_bt<2>(p, st);
+      case 1: return launch_bt<1>(p, st);
       default: break;
     }
   }
