@@ -152,6 +152,12 @@ int fw_plain_create(const fw_plain_desc* desc, int32_t batch, int32_t device, fw
 /* = fast_step (fast.py:216-224): d_in [B] float64 -> d_out [B] float64. */
 int fw_plain_step(fw_handle* h, const double* d_in, double* d_out, void* stream);
 
+/* = naive_step (naive.py:27-110): the sample that extends d_history [n][B] by one,
+ * recomputed cache-free through the demand plan of its receptive field (every demanded
+ * node of a layer in parallel, each in the pinned order of the cached path, so the result
+ * equals it bit for bit). d_out [B]. The queues and the step counter are not touched. */
+int fw_plain_naive(fw_handle* h, const double* d_history, int32_t n, double* d_out, void* stream);
+
 /* = fast_generate's step loop: d_inputs [n_inputs][B], feedback afterwards,
  * d_out [n_steps][B] every step's output. */
 int fw_plain_generate(fw_handle* h, const double* d_inputs, int32_t n_inputs, int32_t n_steps,

@@ -2,6 +2,7 @@
 // weight repacking, queue allocation, argument validation and dispatch.
 #include <cuda_bf16.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -81,10 +82,62 @@ void free_cell(Handle& h) {
 
 void free_plain(Handle& h) {
   void* ptrs[] = {h.p.dil, h.p.cin, h.p.cout, h.p.woff, h.p.boff, h.p.qoff,
-                  h.p.roff, h.p.soff, h.p.taps, h.p.bias, h.p.queue};
+                  h.p.roff, h.p.soff, h.p.taps, h.p.bias, h.p.queue,
+                  h.naive.count, h.naive.goff, h.naive.gather, h.naive.gsrc, h.naive.voff,
+                  h.naive.vals};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   h.p = PlainDev{};
+  h.naive = NaivePlan{};
+}
+
+// The demand plan (reference naive.py:27-110): the top layer at offset 0, layer l-1
+// wherever layer l's taps read it (o + k d_l); nodes in ascending offset order.
+int build_naive_plan(Handle& h) {
+  NaivePlan& pl = h.naive;
+  if (pl.built) return FW_OK;
+  const int n = (int)h.pdil.size(), w = h.p.w;
+  std::vector<std::vector<int64_t>> dem(n);
+  dem[n - 1] = {0};
+  for (int l = n - 1; l > 0; --l) {
+    std::vector<int64_t> v;
+    for (int64_t o : dem[l])
+      for (int k = 0; k < w; ++k) v.push_back(o + (int64_t)k * h.pdil[l]);
+    std::sort(v.begin(), v.end());
+    v.erase(std::unique(v.begin(), v.end()), v.end());
+    dem[l - 1] = v;
+  }
+  std::vector<int> count(n), gather, gsrc;
+  std::vector<int64_t> goff(n), voff(n);
+  int64_t vtot = 0;
+  for (int l = 0; l < n; ++l) {
+    count[l] = (int)dem[l].size();
+    goff[l] = (int64_t)gather.size();
+    voff[l] = vtot;
+    const int cout = l + 1 < n ? h.pcin[l + 1] : 1;
+    vtot += (int64_t)count[l] * cout;
+    for (int64_t o : dem[l])
+      for (int k = 0; k < w; ++k) {
+        const int64_t src = o + (int64_t)k * h.pdil[l];
+        gsrc.push_back((int)src);
+        if (l == 0) {
+          gather.push_back((int)src);
+        } else {
+          auto it = std::lower_bound(dem[l - 1].begin(), dem[l - 1].end(), src);
+          gather.push_back((int)(it - dem[l - 1].begin()));
+        }
+      }
+  }
+  int rc;
+  if ((rc = upload(&pl.count, count.data(), count.size()))) return rc;
+  if ((rc = upload(&pl.goff, goff.data(), goff.size()))) return rc;
+  if ((rc = upload(&pl.gather, gather.data(), gather.size()))) return rc;
+  if ((rc = upload(&pl.gsrc, gsrc.data(), gsrc.size()))) return rc;
+  if ((rc = upload(&pl.voff, voff.data(), voff.size()))) return rc;
+  pl.vals_per_stream = vtot;
+  FW_CUDA(cudaMalloc(&pl.vals, sizeof(double) * (size_t)vtot * h.batch));
+  pl.built = 1;
+  return FW_OK;
 }
 
 int check_handle(const fw_handle* h, bool want_plain) {
@@ -498,6 +551,19 @@ int fw_plain_create(const fw_plain_desc* d, int32_t batch, int32_t device, fw_ha
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(cuda_fail(e, "create synchronize"));
   *out = fh;
+  return FW_OK;
+}
+
+int fw_plain_naive(fw_handle* fh, const double* d_history, int32_t n, double* d_out,
+                   void* stream) {
+  int rc = check_handle(fh, true);
+  if (rc) return rc;
+  if (n < 1) return invalid("the history must hold at least one sample");
+  if (!d_history || !d_out) return invalid("null device buffer");
+  Handle& h = fh->h;
+  FW_CUDA(cudaSetDevice(h.device));
+  if ((rc = build_naive_plan(h))) return rc;
+  FW_CUDA(launch_plain_naive(h, d_history, n, d_out, static_cast<cudaStream_t>(stream)));
   return FW_OK;
 }
 

@@ -118,6 +118,22 @@ cudaError_t launch_plain_compute(const Handle& h, const double* in, const double
                                  double* out, double* states, cudaStream_t st);
 cudaError_t launch_plain_push(const Handle& h, const double* states, cudaStream_t st);
 
+// Cache-free (demand-driven) plain step: the reference's naive_step (naive.py:27-110).
+struct NaivePlan {
+  int built = 0;
+  int* count = nullptr;       // [n] demanded nodes per layer
+  int64_t* goff = nullptr;    // [n] offset of layer l's gather rows in `gather`
+  int* gather = nullptr;      // [nodes][w]: layer 0 -- history offset back from T; l > 0 --
+                              // index of the input node in layer l-1's demanded list
+  int* gsrc = nullptr;        // [nodes][w]: the input's offset back from T (a negative time
+                              // reads zero, as the cached path's zero-filled queues)
+  int64_t* voff = nullptr;    // [n] offset of layer l's node values (per stream)
+  int64_t vals_per_stream = 0;
+  double* vals = nullptr;     // [B][vals_per_stream] scratch
+};
+cudaError_t launch_plain_naive(const Handle& h, const double* history, int n, double* out,
+                               cudaStream_t st);
+
 struct Handle {
   int is_plain = 0;
   int device = 0;
@@ -142,6 +158,7 @@ struct Handle {
   // plain
   PlainDev p{};
   std::vector<int> pdil, pcin;
+  NaivePlan naive{};
 
   // scratch for the *_host entry points
   int32_t* d_io = nullptr;

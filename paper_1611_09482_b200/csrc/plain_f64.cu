@@ -136,6 +136,48 @@ __global__ void plain_push_kernel(PlainParams pp, const double* states) {
   }
 }
 
+// Naive step: every node of the demand plan of the output at T = n-1, layer by layer, each
+// in the same pinned order as eval_layer (so the result equals the queue-cached output bit
+// for bit; pre-history inputs are zero, as the cached path's zero-filled queues).
+__global__ void __launch_bounds__(NT) plain_naive_kernel(PlainDev p, NaivePlan plan, int B,
+                                                         const double* hist, int n, double* out) {
+  const int sidx = blockIdx.x, w = p.w;
+  double* vals = plan.vals + (size_t)sidx * plan.vals_per_stream;
+  const int T = n - 1;
+  for (int l = 0; l < p.n_layers; ++l) {
+    const int cin = p.cin[l], cout = p.cout[l], cnt = plan.count[l];
+    const double* taps = p.taps + p.woff[l];
+    const double* bias = p.bias + p.boff[l];
+    const int* g = plan.gather + plan.goff[l];
+    const int* gs = plan.gsrc + plan.goff[l];
+    double* dst = vals + plan.voff[l];
+    const double* src = l > 0 ? vals + plan.voff[l - 1] : nullptr;
+    for (int e = threadIdx.x; e < cnt * cout; e += NT) {
+      const int node = e / cout, o = e % cout;
+      double acc = 0.0;
+      for (int k = 0; k < w; ++k) {
+        const double* row = taps + ((size_t)k * cout + o) * cin;
+        const int gi = g[node * w + k];
+        if (l == 0) {
+          const int tau = T - gi;  // the scalar input of that time step, zero before it
+          const double v = tau >= 0 ? hist[(size_t)tau * B + sidx] : 0.0;
+          acc = __dadd_rn(acc, __dmul_rn(row[0], v));
+        } else if (T - gs[node * w + k] >= 0) {
+          const double* v = src + (size_t)gi * cin;
+          for (int c = 0; c < cin; ++c) acc = __dadd_rn(acc, __dmul_rn(row[c], v[c]));
+        } else {  // a layer output before the history began: the cached path reads zeros
+          for (int c = 0; c < cin; ++c) acc = __dadd_rn(acc, __dmul_rn(row[c], 0.0));
+        }
+      }
+      acc = __dadd_rn(acc, bias[o]);
+      if (p.act == 1) acc = tanh(acc);
+      dst[(size_t)node * cout + o] = acc;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[sidx] = vals[plan.voff[p.n_layers - 1]];
+}
+
 PlainParams params(const Handle& h) {
   PlainParams pp;
   pp.p = h.p;
@@ -172,6 +214,12 @@ cudaError_t launch_plain_compute(const Handle& h, const double* in, const double
   cudaError_t e = prep((const void*)plain_compute_kernel, sm);
   if (e != cudaSuccess) return e;
   plain_compute_kernel<<<h.batch, NT, sm, st>>>(params(h), in, rec, out, states);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_plain_naive(const Handle& h, const double* history, int n, double* out,
+                               cudaStream_t st) {
+  plain_naive_kernel<<<h.batch, NT, 0, st>>>(h.p, h.naive, h.batch, history, n, out);
   return cudaGetLastError();
 }
 

@@ -93,39 +93,36 @@ def cell_naive_generate(model: CellModel, primer, steps: int, batch: int | None 
 
 # ---- plain mode (the reference's own stack) --------------------------------------------------
 def plain_naive_step(model, history, state=None) -> float:
-    """The reference's naive_step output (naive.py:27-110) for history[-1]: the fast kernel
-    stepped teacher-forced over the receptive-field window from zero queues. The output's
-    demand cone lies inside the window and is evaluated by the same kernel in the same order,
-    so the result equals the queue-cached output bit for bit."""
+    """The reference's naive_step output (naive.py:27-110) for history[-1], recomputed
+    cache-free on the GPU (fw_plain_naive): every node of the demand plan of its receptive
+    field, layer by layer, each in the pinned order of the cached path -- so the result
+    equals the queue-cached output bit for bit. `state` (a GenerationState of this model)
+    lends its handle; its queues are not touched."""
     import ctypes as C
 
     import torch
 
     from . import _lib
     from .fast import init_state
-    from .model import receptive_field
 
     h = np.asarray(history, dtype=np.float64).ravel()
     if h.size == 0:
         raise ValueError("the history must hold at least one sample")
-    rf = receptive_field(model.config)
-    w = h[-rf:]
     own = state is None
     st = init_state(model, 1) if own else state
-    st.reset()
-    x = torch.as_tensor(w.reshape(-1, 1), device=st._dev)
-    out = torch.empty((w.size, 1), dtype=torch.float64, device=st._dev)
-    _lib.check(st._lib.fw_plain_generate(st._h, C.c_void_p(x.data_ptr()), w.size, w.size,
-                                         C.c_void_p(out.data_ptr()), _lib.stream_ptr()))
-    y = float(out[-1, 0].item())
+    x = torch.as_tensor(h.reshape(-1, 1), device=st._dev)
+    y = torch.empty(1, dtype=torch.float64, device=st._dev)
+    _lib.check(st._lib.fw_plain_naive(st._h, C.c_void_p(x.data_ptr()), int(h.size),
+                                      C.c_void_p(y.data_ptr()), _lib.stream_ptr()))
+    out = float(y.item())
     if own:
         st.close()
-    return y
+    return out
 
 
 def plain_naive_generate(model, primer, steps: int):
     """The reference's naive_generate: fast_generate's feedback rule with every output
-    recomputed from the history (cache-free)."""
+    recomputed from the history (cache-free, the demand plan on the GPU)."""
     from .fast import SampleSequence, init_state, scalar_primer
 
     if steps < 0:

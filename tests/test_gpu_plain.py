@@ -131,3 +131,27 @@ def test_generate_zero_steps_is_empty(cuda):
     assert len(fast_generate(m, [0.5], 0)) == 0
     with pytest.raises(ValueError):
         fast_generate(m, [0.5], -1)
+
+
+NAIVE_NAMES = sorted(n for n in NAMES if f"{n}/naive" in G.files)
+
+
+@pytest.mark.parametrize("name", NAIVE_NAMES)
+def test_gpu_naive_matches_reference_naive_generate(cuda, name):
+    """The GPU demand-plan generator (fw_plain_naive) against the
+    unmodified reference's naive_generate on the same primer (golden vectors): bit-exact for
+    linear stacks, tanh within CUDA-vs-glibc ulps; and against the GPU cached path on the
+    same history: bit-exact for every stack (same kernel arithmetic)."""
+    from paper_1611_09482_b200 import naive_generate, naive_step
+
+    m = model_of(name)
+    tanh = m.config.activation == "tanh"
+    primer = G[f"{name}/primer"]
+    want = G[f"{name}/naive"]
+    got = naive_generate(m, primer, len(want))
+    assert got.start_index == len(primer)
+    assert_match(got.scalars(), want, tanh, m.config.total_layers)
+    fast = fast_generate(m, primer, len(want)).scalars()
+    assert np.array_equal(got.scalars(), fast)
+    y, macs = naive_step(m, primer)
+    assert y == fast[0] and macs.node_evaluations >= m.config.total_layers
