@@ -296,7 +296,7 @@ int fw_cell_create(const fw_cell_desc* desc, int32_t batch, int32_t device, int3
   const bool bf = desc->weight_dtype == FW_DTYPE_BF16;
   // queues: layer l holds d_l slots. SIMT: each slot [ceil(B/128)][R/4][128][4] fp32 (R
   // padded to a multiple of 4, streams to a multiple of 128). tcgen05: each slot
-  // [B/64][16][64][8] fp16 -- per 64-stream tile 16 K-pieces of 8 channels (chain_tc.cuh).
+  // [B/128][16][128][8] fp16 -- per 128-stream tile pair 16 K-pieces of 8 channels (chain_tc.cuh).
   // Either way a 128-stream tile's slot is contiguous.
   const int Rp = (R + 3) & ~3;
   const int64_t Bp = ((int64_t)batch + 127) / 128 * 128;

@@ -56,7 +56,10 @@ constexpr int kQueueWarp0 = 10;
 constexpr uint32_t kP1 = 16u << 16;  // lane offset of plane P1
 constexpr uint32_t kColXt = 256, kColXd = 320;  // P0
 constexpr uint32_t kColX = 0, kColZ = 128;      // P1
-constexpr uint32_t kSlotBytes = 16384;  // one tile's ring slot: [16 K-pieces][64 rows][8 fp16]
+constexpr uint32_t kSlotBytes = 16384;  // one tile's share of a ring slot (64 rows x 128 fp16)
+// Ring slots are laid out per tile pair, [16 K-pieces][128 rows][8 fp16] (32 KB): the no-swizzle
+// K-major operand layout of an M = 128 MMA; tile 2p holds rows 0..63, tile 2p+1 rows 64..127.
+constexpr uint32_t kPairRows = 128;
 constexpr uint32_t kStageA = 32768, kStageB = 65536, kStageC = 32768;
 constexpr uint32_t kOffA0 = 0, kOffA1 = kOffA0 + kStageA, kOffB = kOffA1 + kStageA,
                    kOffC = kOffB + kStageB, kOffBars = kOffC + kStageC;
@@ -872,7 +875,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const bool pf = warp == kQueueWarp0 && lane == 0;
     const bool tq = pf;
-    const uint8_t* qtile = a.queue + (size_t)tile * kSlotBytes;
+    const uint8_t* qtile = a.queue + (size_t)(tile >> 1) * 2 * kSlotBytes + (tile & 1) * kChainRows * 16;
     auto qb = [&](int g) { return qbase_of(a, g / L, g % L); };
     // pops: each thread copies its own row of layer g's slot into staging buffer Xq[g & 1]
     // (16 x 16 B, cp.async) two layers ahead -- no registers held across layers, and the
@@ -886,7 +889,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         const uint8_t* src = qtile + qb(g) + (size_t)r * 16;
         const uint32_t dst = smem_u32(xq + (g & 1) * kSlotBytes) + (uint32_t)r * 16;
 #pragma unroll
-        for (int j = 0; j < 16; ++j) cp_async16(dst + (uint32_t)j * kChainRows * 16, src + (size_t)j * kChainRows * 16);
+        for (int j = 0; j < 16; ++j) cp_async16(dst + (uint32_t)j * kChainRows * 16, src + (size_t)j * kPairRows * 16);
       }
       cp_async_commit();
     };
@@ -948,7 +951,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       mbar_wait(xt_ready, par);
       tc_fence_after();
       tmem_to_pieces(kColXt, reinterpret_cast<uint4*>(const_cast<uint8_t*>(qtile) + qb(g)) + r,
-                     kChainRows, act);
+                     kPairRows, act);
       tc_fence_before();
       mbar_arrive(x_pushed);
       if (tq) trace_at(a, l, T_Q_LOAD, clock64());

@@ -136,8 +136,8 @@ __device__ __forceinline__ void st8(__half* p, const V8& x) {
 __device__ __forceinline__ V8 ring_ld8(const Ring& q, int l, int s, int b, int r) {
   if (q.fp16)
     return ld8(reinterpret_cast<const __half*>(q.base + q.off[l] + (int64_t)s * q.slot +
-                                               (int64_t)(b >> 6) * 16384 + (r >> 3) * 1024 +
-                                               (b & 63) * 16));
+                                               (int64_t)(b >> 7) * 32768 + (r >> 3) * 2048 +
+                                               (b & 127) * 16));
   const float* base = reinterpret_cast<const float*>(q.base) + q.off[l] + (int64_t)s * q.slot;
   const float* p0 = base + ((int64_t)((b >> 7) * (q.Rp / 4) + (r >> 2)) * 128 + (b & 127)) * 4;
   const float4 a = *reinterpret_cast<const float4*>(p0), c = *reinterpret_cast<const float4*>(p0 + 512);
@@ -145,8 +145,8 @@ __device__ __forceinline__ V8 ring_ld8(const Ring& q, int l, int s, int b, int r
 }
 __device__ __forceinline__ void ring_st8(const Ring& q, int l, int s, int b, int r, const V8& x) {
   if (q.fp16) {
-    st8(reinterpret_cast<__half*>(q.base + q.off[l] + (int64_t)s * q.slot + (int64_t)(b >> 6) * 16384 +
-                                  (r >> 3) * 1024 + (b & 63) * 16),
+    st8(reinterpret_cast<__half*>(q.base + q.off[l] + (int64_t)s * q.slot + (int64_t)(b >> 7) * 32768 +
+                                  (r >> 3) * 2048 + (b & 127) * 16),
         x);
     return;
   }
