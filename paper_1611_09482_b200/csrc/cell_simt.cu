@@ -21,6 +21,7 @@
 #include <cstdlib>
 
 #include "internal.h"
+#include "tc_ptx.cuh"
 
 namespace fw {
 namespace {
@@ -589,6 +590,422 @@ cudaError_t launch_cluster(const SimtParams& p, cudaStream_t st) {
   return cudaLaunchKernelExC(&cfg, (const void*)cell_cluster_kernel<C>, args);
 }
 
+// ---- K1s: weight-staged fp32 kernel (mid batches, fp32 configs 3 and 5) -----------------
+// The per-CTA kernel above reads every weight with __ldg and spends most of a layer waiting on
+// L2 round trips (cfg5: 13 us per layer for 8 streams, < 10 % of the FP32 pipe). Here a
+// producer warp streams the step's weight matrices, in consumption order, through a ring of
+// shared-memory stages with 1-D bulk copies (TMA engine, mbarrier completion), a GEMV or more
+// ahead of the 8 compute warps, so the L2 latency leaves the layer chain. The compute warps
+// read each weight from shared memory once for all BT streams of the CTA (4 consecutive
+// outputs x BT streams per thread, K split across thread groups and reduced in a fixed order).
+// The ring pops are prefetched two layers ahead by the threads that push the same elements
+// (cp.async: program order covers the slot reuse, as in the tcgen05 chain). Same cell, same
+// pop -> compute -> push order per layer as cell_simt_kernel (fast.py:131-213).
+constexpr int kStNT = 256;                 // compute threads (8 warps)
+constexpr int kStThreads = kStNT + 32;     // + the weight producer warp
+constexpr int kStStagesMax = 8;            // weight ring depth (runtime, <= 8)
+constexpr int kStBarId = 1;                // named barrier of the compute warps
+
+struct StagedLayout {
+  int stage_bytes;  // one weight stage
+  int issuers;      // producer lanes issuing a chunk's bulk copies
+  int stages;       // ring depth
+  int exp;          // measurement only: 1 = the producer skips the weight copies
+  // float offsets of the activation buffers from the start of dynamic smem
+  int xx, a, z, s, hb, lg, red, pops, bias, hbias, lcon, cls, ring, bars;
+  size_t total;
+};
+
+// rows of a [K][N] fp32 weight matrix per stage (a multiple of 4)
+__host__ __device__ __forceinline__ int st_rows(int K, int N, int stage_bytes) {
+  const int r = (stage_bytes / (N * 4)) & ~3;
+  return r < K ? r : K;
+}
+
+struct StageRing {
+  uint64_t* full;
+  uint64_t* empty;
+  float* buf;
+  int stage_floats;
+  int slot;
+  uint32_t ph;
+  uint32_t crank, csize;  // cluster rank / size: each CTA loads 1/csize of a stage, multicast
+  int nst;                // stages in the ring
+  __device__ __forceinline__ void advance() {
+    if (++slot == nst) {
+      slot = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+// Producer side of one GEMV: its K-chunks into the ring, run by the whole producer warp.
+// A chunk is split into `issuers` bulk copies issued by different lanes (one thread's bulk
+// copies execute one after another); with a cluster each CTA loads 1/csize of every slice and
+// multicasts it to the cluster.
+__device__ __forceinline__ void st_produce(StageRing& rg, const float* W, int K, int N,
+                                           int stage_bytes, int issuers) {
+  const int lane = threadIdx.x & 31;
+  const int kc = st_rows(K, N, stage_bytes);
+  for (int k0 = 0; k0 < K; k0 += kc) {
+    const int rows = min(kc, K - k0);
+    const uint32_t bytes = (uint32_t)rows * N * 4;
+    if (lane == 0) {
+      // the slot is free once every compute warp of every CTA of the cluster released it
+      if (rg.csize == 1) ptx::mbar_wait(&rg.empty[rg.slot], rg.ph ^ 1u);
+      else ptx::mbar_wait_cluster(&rg.empty[rg.slot], rg.ph ^ 1u);
+      if (issuers == 0) ptx::mbar_arrive(&rg.full[rg.slot]);
+      else ptx::mbar_arrive_expect_tx(&rg.full[rg.slot], bytes);
+    }
+    __syncwarp();
+    const uint32_t parts = rg.csize * (uint32_t)max(issuers, 1);
+    const uint32_t slice = (bytes + 16 * parts - 1) / (16 * parts) * 16;
+    const uint32_t off = (rg.crank * (uint32_t)issuers + (uint32_t)lane) * slice;
+    if (lane < issuers && off < bytes) {  // (issuers == 0: measurement, no copies)
+      const uint32_t n = min(slice, bytes - off);
+      uint8_t* dst = reinterpret_cast<uint8_t*>(rg.buf + (size_t)rg.slot * rg.stage_floats) + off;
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(W + (size_t)k0 * N) + off;
+      if (rg.csize == 1) {
+        ptx::bulk_g2s(dst, src, n, &rg.full[rg.slot]);
+      } else {
+        const uint16_t mask = (uint16_t)((1u << rg.csize) - 1u);
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+            " [%0], [%1], %2, [%3], %4;" ::"r"(ptx::smem_u32(dst)),
+            "l"(src), "r"(n), "r"(ptx::smem_u32(&rg.full[rg.slot])), "h"(mask)
+            : "memory");
+      }
+    }
+    rg.advance();
+  }
+}
+
+// Consumer side: out[b][o] = epi(b, o, sum_k W[k][o] in[b][k]) for b < BT, o < N (N % 4 == 0,
+// N <= 1024, K % 4 == 0, ldin % 4 == 0). Ends with a barrier of the compute warps.
+template <int BT, typename Epi>
+__device__ __forceinline__ void st_gemv(StageRing& rg, const float* in, int ldin, int K, int N,
+                                        int stage_bytes, float* red, Epi epi) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int NQ = N >> 2;
+  const int G = NQ >= kStNT ? 1 : kStNT / NQ;
+  const int q = tid % NQ, g = tid / NQ;
+  const bool on = g < G && q < NQ;
+  float acc[4][BT];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int b = 0; b < BT; ++b) acc[j][b] = 0.f;
+  const int kc = st_rows(K, N, stage_bytes);
+  for (int k0 = 0; k0 < K; k0 += kc) {
+    const int rows = min(kc, K - k0);
+    const int rpg = ((rows + G - 1) / G + 3) & ~3;
+    ptx::mbar_wait(&rg.full[rg.slot], rg.ph);
+    const float* w = rg.buf + (size_t)rg.slot * rg.stage_floats;
+    if (on) {
+      const int ka = g * rpg, kb = min(rows, ka + rpg);
+      for (int k = ka; k < kb; k += 4) {
+        float4 wv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) wv[u] = *reinterpret_cast<const float4*>(w + (size_t)(k + u) * N + 4 * q);
+#pragma unroll
+        for (int b = 0; b < BT; ++b) {
+          const float4 x = *reinterpret_cast<const float4*>(in + b * ldin + k0 + k);
+          const float xs[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            acc[0][b] = fmaf(wv[u].x, xs[u], acc[0][b]);
+            acc[1][b] = fmaf(wv[u].y, xs[u], acc[1][b]);
+            acc[2][b] = fmaf(wv[u].z, xs[u], acc[2][b]);
+            acc[3][b] = fmaf(wv[u].w, xs[u], acc[3][b]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    // (a cluster-scope release waits for the warp's outstanding global stores: without a
+    // cluster the CTA-scope arrive keeps the ring pushes off the chain)
+    if (rg.csize == 1) {
+      if (lane == 0) ptx::mbar_arrive(&rg.empty[rg.slot]);
+    } else if (lane < (int)rg.csize) {
+      ptx::mbar_arrive_remote(ptx::mapa(&rg.empty[rg.slot], (uint32_t)lane));
+    }
+    rg.advance();
+  }
+  if (G == 1) {
+    if (on)
+#pragma unroll
+      for (int b = 0; b < BT; ++b)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) epi(b, 4 * q + j, acc[j][b]);
+  } else {
+    if (on)
+#pragma unroll
+      for (int b = 0; b < BT; ++b)
+        *reinterpret_cast<float4*>(red + ((size_t)g * BT + b) * N + 4 * q) =
+            make_float4(acc[0][b], acc[1][b], acc[2][b], acc[3][b]);
+    ptx::named_bar_sync(kStBarId, kStNT);
+    for (int e = tid; e < BT * N; e += kStNT) {
+      float v = 0.f;
+      for (int gg = 0; gg < G; ++gg) v += red[(size_t)gg * BT * N + e];
+      epi(e / N, e % N, v);
+    }
+  }
+  ptx::named_bar_sync(kStBarId, kStNT);
+}
+
+template <int BT>
+StagedLayout staged_layout(const CellDims& d, int stages = 3) {
+  StagedLayout y{};
+  y.stages = stages;
+  int o = 0;
+  auto take = [&](int floats) {
+    const int at = o;
+    o += (floats + 31) & ~31;  // 128-byte aligned buffers
+    return at;
+  };
+  y.xx = take(BT * 2 * d.R);
+  y.a = take(BT * 2 * d.D);
+  y.z = take(BT * d.D);
+  y.s = take(BT * d.S);
+  y.hb = take(BT * d.H);
+  y.lg = take(BT * d.A);
+  y.red = take(kStNT * 4 * BT);
+  y.pops = take(3 * BT * d.R);
+  y.bias = take(3 * (2 * d.D + d.S + d.R));  // per-layer biases, prefetched with the pops
+  y.hbias = take(d.H + d.A);
+  y.lcon = take(3 * d.L);                    // per-layer ring offsets (int64) and dilations
+  y.cls = take(BT);
+  y.bars = take(2 * 2 * kStStagesMax);
+  y.ring = take(0);
+  const size_t budget = 227 * 1024 - 1024;
+  const size_t used = (size_t)y.ring * 4;
+  y.stage_bytes = used >= budget ? 0 : (int)(((budget - used) / stages) & ~(size_t)1023);
+  y.total = used + (size_t)stages * y.stage_bytes;
+  return y;
+}
+
+template <int BT>
+__global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p, StagedLayout y) {
+  extern __shared__ __align__(1024) float smf[];
+  const CellDims d = p.d;
+  const int R = d.R, D = d.D, S = d.S, H = d.H, A = d.A, L = d.L;
+  float* xx = smf + y.xx;  // [BT][2R]: x_l[t] | x_l[t-d]
+  float* a = smf + y.a;    // [BT][2D]
+  float* z = smf + y.z;    // [BT][D]
+  float* s = smf + y.s;    // [BT][S]
+  float* hb = smf + y.hb;  // [BT][H]
+  float* lg = smf + y.lg;  // [BT][A]
+  float* red = smf + y.red;
+  float* pops = smf + y.pops;  // [3][BT][R]: x_{t-d} of layers g, g+1, g+2
+  // [3][2D | S | R]: dil / skip / res biases of layers g, g+1, g+2 (global loads in the
+  // epilogues would put an L2 round trip per GEMV on the chain)
+  float* bias = smf + y.bias;
+  float* hbias = smf + y.hbias;  // h1 | h2 biases
+  int64_t* qoff_s = reinterpret_cast<int64_t*>(smf + y.lcon);
+  int* dil_s = reinterpret_cast<int*>(qoff_s + L);
+  const int NB = 2 * D + S + R;
+  int* cls = reinterpret_cast<int*>(smf + y.cls);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smf + y.bars);
+  StageRing rg{bars, bars + kStStagesMax, smf + y.ring, y.stage_bytes / 4, 0, 0u,
+               ptx::cluster_rank(), ptx::cluster_size(), y.stages};
+
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int s0 = blockIdx.x * BT;
+  const int nb = min(BT, p.B - s0);
+  const CellRun& run = p.run;
+  const int B = p.B;
+  const int sb = y.stage_bytes;
+  if (tid == 0) {
+    for (int i = 0; i < rg.nst; ++i) {
+      ptx::mbar_init(&rg.full[i], 1);
+      ptx::mbar_init(&rg.empty[i], kStNT / 32 * rg.csize);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (tid < BT) cls[tid] = (tid < nb) ? run.inputs[s0 + tid] : 0;
+  for (int e = tid; e < L; e += blockDim.x) {
+    qoff_s[e] = p.qoff[e];
+    dil_s[e] = p.dil[e];
+  }
+  for (int e = tid; e < H + A; e += blockDim.x) hbias[e] = e < H ? p.w.h1_b[e] : p.w.h2_b[e - H];
+  if (rg.csize > 1) ptx::cluster_sync();  // every CTA's barriers exist before any multicast
+  else __syncthreads();
+
+  if (warp == kStNT / 32) {
+    // ---- weight producer: the step's GEMVs in the compute warps' order ----
+    const int is = y.exp == 1 ? 0 : y.issuers;
+    for (int i = 0; i < run.n_steps; ++i) {
+      for (int l = 0; l < L; ++l) {
+        st_produce(rg, p.w.dilT + (size_t)l * 2 * R * 2 * D, 2 * R, 2 * D, sb, is);
+        st_produce(rg, p.w.skipT + (size_t)l * D * S, D, S, sb, is);
+        if (l + 1 < L) st_produce(rg, p.w.resT + (size_t)l * D * R, D, R, sb, is);
+      }
+      st_produce(rg, p.w.h1T, S, H, sb, is);
+      st_produce(rg, p.w.h2T, H, A, sb, is);
+    }
+    __syncwarp();
+    if (rg.csize > 1) ptx::cluster_sync();  // the peers' multicasts and arrivals are done
+    return;
+  }
+
+  // ring pops: thread e owns (stream b, 4-channel chunk c4) for every layer -- it pushes the
+  // chunk and prefetches the same chunk of the layer two ahead
+  const int Rp = (R + 3) & ~3;
+  const int R4 = R >> 2;  // R % 4 == 0 here
+  const size_t slot_elems = (size_t)((B + 127) / 128) * 128 * Rp;
+  const int G = run.n_steps * L;
+  auto slot_ptr = [&](int gg, int b, int c4) {
+    const int l = gg % L;
+    const int64_t t = run.t0 + gg / L;
+    const int st = s0 + b;
+    return p.queue + qoff_s[l] + (size_t)(t % dil_s[l]) * slot_elems +
+           ((size_t)((st >> 7) * (Rp / 4) + c4) * 128 + (st & 127)) * 4;
+  };
+  auto prefetch = [&](int gg) {
+    if (gg < G) {
+      for (int e = tid; e < nb * R4; e += kStNT) {
+        const int b = e / R4, c4 = e % R4;
+        ptx::cp_async16(ptx::smem_u32(pops + ((gg % 3) * BT + b) * R + 4 * c4), slot_ptr(gg, b, c4));
+      }
+      const int l = gg % L;
+      float* bb = bias + (gg % 3) * NB;
+      for (int e = tid; e < NB / 4; e += kStNT) {
+        const int o = 4 * e;
+        const float* src = o < 2 * D ? p.w.dil_b + (size_t)l * 2 * D + o
+                         : o < 2 * D + S ? p.w.skip_b + (size_t)l * S + (o - 2 * D)
+                                         : p.w.res_b + (size_t)l * R + (o - 2 * D - S);
+        ptx::cp_async16(ptx::smem_u32(bb + o), src);
+      }
+    }
+    ptx::cp_async_commit();
+  };
+  prefetch(0);
+  prefetch(1);
+
+  // measurement only (FW_SIMT_EXP=2): thread 0 of CTA 0 prints one layer's phase cycles
+  const bool trace = y.exp == 2 && blockIdx.x == 0 && tid == 0;
+  long long stamp[8];
+  for (int i = 0; i < run.n_steps; ++i) {
+    const int64_t t = run.t0 + i;
+    if (trace) stamp[7] = clock64();
+    for (int e = tid; e < BT * R; e += kStNT) {
+      const int b = e / R, r = e % R;
+      xx[b * 2 * R + r] = __ldg(p.w.embed + (size_t)cls[b] * R + r);
+    }
+    for (int e = tid; e < BT * S; e += kStNT) s[e] = 0.f;
+    ptx::named_bar_sync(kStBarId, kStNT);
+    for (int l = 0; l < L; ++l) {
+      const int gg = i * L + l;
+      if (trace) stamp[0] = clock64();
+      // pop + push on slot t mod d_l (fast.py:131-147, 200-213): x_l[t-d] from the prefetch,
+      // x_l[t] into the slot
+      ptx::cp_async_wait<1>();
+      if (trace) stamp[1] = clock64();
+      for (int e = tid; e < nb * R4; e += kStNT) {
+        const int b = e / R4, c4 = e % R4;
+        const float4 old = *reinterpret_cast<const float4*>(pops + ((gg % 3) * BT + b) * R + 4 * c4);
+        *reinterpret_cast<float4*>(xx + b * 2 * R + R + 4 * c4) = old;
+        *reinterpret_cast<float4*>(slot_ptr(gg, b, c4)) =
+            *reinterpret_cast<const float4*>(xx + b * 2 * R + 4 * c4);
+      }
+      prefetch(gg + 2);
+      ptx::named_bar_sync(kStBarId, kStNT);
+      if (trace) stamp[2] = clock64();
+      const float* db = bias + (gg % 3) * NB;
+      st_gemv<BT>(rg, xx, 2 * R, 2 * R, 2 * D, sb, red,
+                  [&](int b, int o, float v) { a[b * 2 * D + o] = v + db[o]; });
+      if (trace) stamp[3] = clock64();
+      for (int e = tid; e < BT * D; e += kStNT) {
+        const int b = e / D, j = e % D;
+        z[e] = tanhf(a[b * 2 * D + j]) * sigmoidf_(a[b * 2 * D + D + j]);
+      }
+      ptx::named_bar_sync(kStBarId, kStNT);
+      if (trace) stamp[4] = clock64();
+      const float* sbias = bias + (gg % 3) * NB + 2 * D;
+      st_gemv<BT>(rg, z, D, D, S, sb, red,
+                  [&](int b, int o, float v) { s[b * S + o] += v + sbias[o]; });
+      if (trace) stamp[5] = clock64();
+      if (l + 1 < L) {
+        const float* rb = bias + (gg % 3) * NB + 2 * D + S;
+        st_gemv<BT>(rg, z, D, D, R, sb, red,
+                    [&](int b, int o, float v) { xx[b * 2 * R + o] += v + rb[o]; });
+      }
+      if (trace) stamp[6] = clock64();
+      if (trace && l == 5 && i == 3)
+        printf("staged trace l5: wait_pop %lld push %lld dil %lld gate %lld skip %lld res %lld\n",
+               stamp[1] - stamp[0], stamp[2] - stamp[1], stamp[3] - stamp[2], stamp[4] - stamp[3],
+               stamp[5] - stamp[4], stamp[6] - stamp[5]);
+    }
+    // head: logits = W2 relu(W1 relu(s) + b1) + b2
+    for (int e = tid; e < BT * S; e += kStNT) s[e] = fmaxf(s[e], 0.f);
+    ptx::named_bar_sync(kStBarId, kStNT);
+    st_gemv<BT>(rg, s, S, S, H, sb, red,
+                [&](int b, int o, float v) { hb[b * H + o] = fmaxf(v + hbias[o], 0.f); });
+    st_gemv<BT>(rg, hb, H, H, A, sb, red,
+                [&](int b, int o, float v) { lg[b * A + o] = v + hbias[H + o]; });
+    if (run.logits != nullptr && i < run.n_logit_steps) {
+      float* dst = run.logits + ((size_t)i * B + s0) * A;
+      for (int e = tid; e < nb * A; e += kStNT) dst[e] = lg[e];
+    }
+    for (int b = warp; b < nb; b += kStNT / 32) {
+      const uint32_t gs = (uint32_t)(run.stream_offset + s0 + b);
+      const uint32_t prefix = noise_prefix(run.seed, gs, (uint32_t)t);
+      const int c = select_class(lg + b * A, A, run.mode, prefix);
+      if ((tid & 31) == 0) {
+        run.out[(size_t)i * B + s0 + b] = c;
+        cls[b] = (i + 1 < run.n_inputs) ? run.inputs[(size_t)(i + 1) * B + s0 + b] : c;
+      }
+    }
+    ptx::named_bar_sync(kStBarId, kStNT);
+  }
+  ptx::cp_async_wait<0>();
+  if (rg.csize > 1) ptx::cluster_sync();
+}
+
+bool staged_supported(const CellDims& d) {
+  auto m4 = [](int v) { return v % 4 == 0; };
+  return d.L >= 3 && m4(d.R) && m4(d.D) && m4(d.S) && m4(d.H) && m4(d.A) && 2 * d.D <= 1024 &&
+         d.S <= 1024 && d.H <= 1024 && d.A <= 1024 && d.R <= 1024 &&
+         staged_layout<8>(d).stage_bytes >= 4 * 4 * 1024;
+}
+
+template <int BT>
+cudaError_t launch_staged(const SimtParams& p, cudaStream_t st) {
+  int stages = 3;
+  if (const char* ev = getenv("FW_SIMT_STAGES")) stages = max(2, min(kStStagesMax, atoi(ev)));
+  StagedLayout y = staged_layout<BT>(p.d, stages);
+  if (y.stage_bytes < 4 * 4 * 1024) y = staged_layout<BT>(p.d, 3);
+  y.issuers = 4;
+  if (const char* ev = getenv("FW_SIMT_EXP")) y.exp = atoi(ev);
+  if (const char* ev = getenv("FW_SIMT_ISSUERS")) y.issuers = max(1, min(32, atoi(ev)));
+  cudaError_t e = cudaFuncSetAttribute(cell_staged_kernel<BT>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)y.total);
+  if (e != cudaSuccess) return e;
+  // clusters of C CTAs share each weight stage (multicast): L2 serves 1/C of the bytes
+  int C = 1;
+  if (const char* ev = getenv("FW_SIMT_MCAST")) C = atoi(ev);
+  if (C != 1 && C != 2 && C != 4 && C != 8) C = 1;
+  const int grid = ((p.B + BT - 1) / BT + C - 1) / C * C;
+  if (C == 1) {
+    cell_staged_kernel<BT><<<grid, kStThreads, y.total, st>>>(p, y);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kStThreads);
+  cfg.dynamicSmemBytes = y.total;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  void* args[] = {const_cast<SimtParams*>(&p), const_cast<StagedLayout*>(&y)};
+  return cudaLaunchKernelExC(&cfg, (const void*)cell_staged_kernel<BT>, args);
+}
+
 constexpr size_t kPrePopMax = 64 * 1024;  // bytes of smem the pre-pop buffer may take
 
 template <int BT>
@@ -638,6 +1055,23 @@ cudaError_t launch_cell_simt(const Handle& h, const CellRun& run, cudaStream_t s
       case 4: return launch_cluster<4>(p, st);
       case 2: return launch_cluster<2>(p, st);
       default: break;
+    }
+  }
+  // mid/large batches: the weight-staged kernel (FW_SIMT_STAGED=0 selects the __ldg kernel)
+  const char* se = getenv("FW_SIMT_STAGED");
+  if (staged_supported(h.dims) && !(se != nullptr && atoi(se) == 0)) {
+    int bt = 8;
+    for (int c : {1, 2, 4, 8})
+      if ((B + c - 1) / c <= 148) {
+        bt = c;
+        break;
+      }
+    if (const char* e = getenv("FW_SIMT_BT")) bt = atoi(e);
+    switch (bt) {
+      case 1: return launch_staged<1>(p, st);
+      case 2: return launch_staged<2>(p, st);
+      case 4: return launch_staged<4>(p, st);
+      default: return launch_staged<8>(p, st);
     }
   }
   if (const char* e = getenv("FW_SIMT_BT")) {  // streams per CTA override (measurements)

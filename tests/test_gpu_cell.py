@@ -319,3 +319,31 @@ def test_tcgen05_padded_batch(cuda, B):
     assert pf.shape == (6, B, 256)
     assert np.max(np.abs(pf.cpu().numpy() - lg)) <= 2e-2
     assert gen.step_index == 6
+
+
+@pytest.mark.parametrize("bt", ["1", "2", "4", "8"])
+def test_staged_simt_kernel_matches_oracle_and_ldg_kernel(cuda, monkeypatch, bt):
+    """The weight-staged fp32 kernel (bulk-copied weight ring, FW_SIMT_BT streams per CTA, the
+    last CTA partly filled) gives the oracle's teacher-forced logits, including shapes whose
+    GEMVs span several stages (R = 128, S = H = 512) and non-zero biases, and continues a
+    free run with the __ldg kernel's classes."""
+    monkeypatch.setenv("FW_SIMT_BT", bt)
+    for cfg, B in ((CellConfig(2, 3, 64, 64, 256, bias="fan_in", init_seed=4), 37),
+                   (CellConfig(1, 4, 128, 128, 512, bias="fan_in", init_seed=6), 19)):
+        m = build_cell_model(cfg)
+        n = 24
+        cls = np.random.default_rng(7).integers(0, 256, (n, B))
+        monkeypatch.setenv("FW_SIMT_STAGED", "1")
+        out, lg = run(CellGenerator(m, B, kernel="simt"), cls, n, Sampler(0), n)
+        o = oc.CellOracle(m)
+        for b in (0, B // 2, B - 1):
+            ref = o.forward_full(cls[:, b])
+            assert np.max(np.abs(lg[:, b] - ref)) <= 1e-4, (bt, B, b)
+        primer = cls[:3]
+        s = Sampler(configs.SAMPLE_GUMBEL, 11)
+        got, _ = run(CellGenerator(m, B, kernel="simt"), primer, 40, s, 0)
+        monkeypatch.setenv("FW_SIMT_STAGED", "0")
+        monkeypatch.delenv("FW_SIMT_BT")
+        want, _ = run(CellGenerator(m, B, kernel="simt"), primer, 40, s, 0)
+        monkeypatch.setenv("FW_SIMT_BT", bt)
+        assert (got != want).mean() < 0.02  # near-ties may flip a class, not the run
