@@ -63,7 +63,7 @@ std::vector<float> maybe_round(const float* src, size_t n, bool bf16) {
 
 void free_cell(Handle& h) {
   float** ptrs[] = {&h.w.embed, &h.w.dilT, &h.w.dil_b, &h.w.resT, &h.w.res_b, &h.w.skipT,
-                    &h.w.skip_b, &h.w.h1T, &h.w.h1_b, &h.w.h2T, &h.w.h2_b, &h.d_queue};
+                    &h.w.catT, &h.w.skip_b, &h.w.h1T, &h.w.h1_b, &h.w.h2T, &h.w.h2_b, &h.d_queue};
   for (float** p : ptrs) {
     if (*p) cudaFree(*p);
     *p = nullptr;
@@ -345,6 +345,14 @@ int fw_cell_create(const fw_cell_desc* desc, int32_t batch, int32_t device, int3
     if ((rc = upload(&h.w.resT, resT.data(), resT.size()))) return fail(rc);
     if ((rc = upload(&h.w.res_b, res_b.data(), res_b.size()))) return fail(rc);
     if ((rc = upload(&h.w.skipT, skipT.data(), skipT.size()))) return fail(rc);
+    {
+      std::vector<float> catT((size_t)L * D * (S + R));
+      for (size_t row = 0; row < (size_t)L * D; ++row) {
+        std::memcpy(catT.data() + row * (S + R), skipT.data() + row * S, sizeof(float) * S);
+        std::memcpy(catT.data() + row * (S + R) + S, resT.data() + row * R, sizeof(float) * R);
+      }
+      if ((rc = upload(&h.w.catT, catT.data(), catT.size()))) return fail(rc);
+    }
     if ((rc = upload(&h.w.skip_b, skip_b.data(), skip_b.size()))) return fail(rc);
     if ((rc = upload(&h.w.h1T, h1T.data(), h1T.size()))) return fail(rc);
     if ((rc = upload(&h.w.h1_b, h1_b.data(), h1_b.size()))) return fail(rc);

@@ -612,7 +612,7 @@ struct StagedLayout {
   int stages;       // ring depth
   int exp;          // measurement only: 1 = the producer skips the weight copies
   // float offsets of the activation buffers from the start of dynamic smem
-  int xx, a, z, s, hb, lg, red, pops, bias, hbias, lcon, cls, ring, bars;
+  int xx, z, s, hb, lg, red, pops, bias, hbias, lcon, cls, ring, bars;
   size_t total;
 };
 
@@ -680,75 +680,135 @@ __device__ __forceinline__ void st_produce(StageRing& rg, const float* W, int K,
   }
 }
 
-// Consumer side: out[b][o] = epi(b, o, sum_k W[k][o] in[b][k]) for b < BT, o < N (N % 4 == 0,
-// N <= 1024, K % 4 == 0, ldin % 4 == 0). Ends with a barrier of the compute warps.
-template <int BT, typename Epi>
-__device__ __forceinline__ void st_gemv(StageRing& rg, const float* in, int ldin, int K, int N,
-                                        int stage_bytes, float* red, Epi epi) {
+// Consumer side, part 1: partial sums of out[b][o] = sum_k W[k][o] in[b][k] (b < BT, o < N,
+// N % 4 == 0, K % 4 == 0, ldin % 4 == 0) into red[g][b][o], one slice per K group g of the
+// thread groups (4 consecutive outputs x BT streams per thread). Returns the group count;
+// ends with a barrier of the compute warps.
+template <int BT, int OB>
+__device__ __forceinline__ int st_partial_ob(StageRing& rg, const float* in, int ldin, int K, int N,
+                                          int stage_bytes, float* red) {
   const int tid = threadIdx.x, lane = tid & 31;
-  const int NQ = N >> 2;
+  const int NQ = N / OB;
   const int G = NQ >= kStNT ? 1 : kStNT / NQ;
-  const int q = tid % NQ, g = tid / NQ;
-  const bool on = g < G && q < NQ;
-  float acc[4][BT];
+  float acc[OB][BT];
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
+  for (int j = 0; j < OB; ++j)
 #pragma unroll
     for (int b = 0; b < BT; ++b) acc[j][b] = 0.f;
   const int kc = st_rows(K, N, stage_bytes);
-  for (int k0 = 0; k0 < K; k0 += kc) {
-    const int rows = min(kc, K - k0);
-    const int rpg = ((rows + G - 1) / G + 3) & ~3;
-    ptx::mbar_wait(&rg.full[rg.slot], rg.ph);
-    const float* w = rg.buf + (size_t)rg.slot * rg.stage_floats;
-    if (on) {
+  for (int qq = tid; qq < NQ * G; qq += kStNT) {  // one pass unless N > 4 * kStNT
+    const int q = qq % NQ, g = qq / NQ;
+    for (int k0 = 0; k0 < K; k0 += kc) {
+      const int rows = min(kc, K - k0);
+      const int rpg = ((rows + G - 1) / G + 3) & ~3;
+      if (qq == tid) ptx::mbar_wait(&rg.full[rg.slot], rg.ph);
+      const float* w = rg.buf + (size_t)rg.slot * rg.stage_floats;
       const int ka = g * rpg, kb = min(rows, ka + rpg);
       for (int k = ka; k < kb; k += 4) {
-        float4 wv[4];
+        float wv[4][OB];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) wv[u] = *reinterpret_cast<const float4*>(w + (size_t)(k + u) * N + 4 * q);
+        for (int u = 0; u < 4; ++u) {
+          const float* wr = w + (size_t)(k + u) * N + OB * q;
+          if constexpr (OB == 4) {
+            const float4 t4 = *reinterpret_cast<const float4*>(wr);
+            wv[u][0] = t4.x, wv[u][1] = t4.y, wv[u][2] = t4.z, wv[u][3] = t4.w;
+          } else if constexpr (OB == 2) {
+            const float2 t2 = *reinterpret_cast<const float2*>(wr);
+            wv[u][0] = t2.x, wv[u][1] = t2.y;
+          } else {
+            wv[u][0] = *wr;
+          }
+        }
 #pragma unroll
         for (int b = 0; b < BT; ++b) {
           const float4 x = *reinterpret_cast<const float4*>(in + b * ldin + k0 + k);
           const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            acc[0][b] = fmaf(wv[u].x, xs[u], acc[0][b]);
-            acc[1][b] = fmaf(wv[u].y, xs[u], acc[1][b]);
-            acc[2][b] = fmaf(wv[u].z, xs[u], acc[2][b]);
-            acc[3][b] = fmaf(wv[u].w, xs[u], acc[3][b]);
-          }
+          for (int u = 0; u < 4; ++u)
+#pragma unroll
+            for (int j = 0; j < OB; ++j) acc[j][b] = fmaf(wv[u][j], xs[u], acc[j][b]);
         }
       }
+      if (qq == tid) {
+        // (a cluster-scope release waits for the warp's outstanding global stores: without a
+        // cluster the CTA-scope arrive keeps the ring pushes off the chain)
+        __syncwarp();
+        if (rg.csize == 1) {
+          if (lane == 0) ptx::mbar_arrive(&rg.empty[rg.slot]);
+        } else if (lane < (int)rg.csize) {
+          ptx::mbar_arrive_remote(ptx::mapa(&rg.empty[rg.slot], (uint32_t)lane));
+        }
+        rg.advance();
+      }
     }
-    __syncwarp();
-    // (a cluster-scope release waits for the warp's outstanding global stores: without a
-    // cluster the CTA-scope arrive keeps the ring pushes off the chain)
-    if (rg.csize == 1) {
-      if (lane == 0) ptx::mbar_arrive(&rg.empty[rg.slot]);
-    } else if (lane < (int)rg.csize) {
-      ptx::mbar_arrive_remote(ptx::mapa(&rg.empty[rg.slot], (uint32_t)lane));
+#pragma unroll
+    for (int b = 0; b < BT; ++b) {
+#pragma unroll
+      for (int j = 0; j < OB; ++j) {
+        red[((size_t)g * BT + b) * N + OB * q + j] = acc[j][b];
+        acc[j][b] = 0.f;
+      }
     }
-    rg.advance();
   }
-  if (G == 1) {
-    if (on)
-#pragma unroll
-      for (int b = 0; b < BT; ++b)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) epi(b, 4 * q + j, acc[j][b]);
-  } else {
-    if (on)
-#pragma unroll
-      for (int b = 0; b < BT; ++b)
-        *reinterpret_cast<float4*>(red + ((size_t)g * BT + b) * N + 4 * q) =
-            make_float4(acc[0][b], acc[1][b], acc[2][b], acc[3][b]);
-    ptx::named_bar_sync(kStBarId, kStNT);
-    for (int e = tid; e < BT * N; e += kStNT) {
-      float v = 0.f;
-      for (int gg = 0; gg < G; ++gg) v += red[(size_t)gg * BT * N + e];
-      epi(e / N, e % N, v);
+  if (NQ * G < kStNT && tid >= NQ * G) {
+    // idle threads still walk the ring
+    for (int k0 = 0; k0 < K; k0 += kc) {
+      ptx::mbar_wait(&rg.full[rg.slot], rg.ph);
+      __syncwarp();
+      if (rg.csize == 1) {
+        if (lane == 0) ptx::mbar_arrive(&rg.empty[rg.slot]);
+      } else if (lane < (int)rg.csize) {
+        ptx::mbar_arrive_remote(ptx::mapa(&rg.empty[rg.slot], (uint32_t)lane));
+      }
+      rg.advance();
     }
+  }
+  ptx::named_bar_sync(kStBarId, kStNT);
+  return G;
+}
+
+// outputs per thread: 4 (fewest shared-memory loads per FMA) once BT >= 4 streams share each
+// weight; at 1-2 streams the phase is latency-bound and as few outputs as keep N / OB <= kStNT
+// leave fewer K groups to reduce (measured: cfg5 729 vs 790 us/step at BT = 8)
+template <int BT>
+__device__ __forceinline__ int st_partial(StageRing& rg, const float* in, int ldin, int K, int N,
+                                          int stage_bytes, float* red) {
+  if (BT >= 4) return st_partial_ob<BT, 4>(rg, in, ldin, K, N, stage_bytes, red);
+  if (N <= kStNT) return st_partial_ob<BT, 1>(rg, in, ldin, K, N, stage_bytes, red);
+  if (N <= 2 * kStNT) return st_partial_ob<BT, 2>(rg, in, ldin, K, N, stage_bytes, red);
+  return st_partial_ob<BT, 4>(rg, in, ldin, K, N, stage_bytes, red);
+}
+
+// fixed-order sum of the K groups' partials of the 4 elements at e4 = b * N + 4 q
+__device__ __forceinline__ float4 st_sum4(const float* red, int G, int BTN, int e4) {
+  float4 v = *reinterpret_cast<const float4*>(red + e4);
+  for (int g = 1; g < G; ++g) {
+    const float4 u = *reinterpret_cast<const float4*>(red + (size_t)g * BTN + e4);
+    v.x += u.x;
+    v.y += u.y;
+    v.z += u.z;
+    v.w += u.w;
+  }
+  return v;
+}
+__device__ __forceinline__ float4 add4(float4 a, float4 b) {
+  return make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+}
+__device__ __forceinline__ float4 relu4(float4 a) {
+  return make_float4(fmaxf(a.x, 0.f), fmaxf(a.y, 0.f), fmaxf(a.z, 0.f), fmaxf(a.w, 0.f));
+}
+#define ST_F4(p) (*reinterpret_cast<float4*>(p))
+#define ST_C4(p) (*reinterpret_cast<const float4*>(p))
+
+// Part 2 for the head GEMVs: reduce + epilogue over 4 outputs at a time, then a barrier.
+template <int BT, typename Epi>
+__device__ __forceinline__ void st_gemv(StageRing& rg, const float* in, int ldin, int K, int N,
+                                        int stage_bytes, float* red, Epi epi) {
+  const int G = st_partial<BT>(rg, in, ldin, K, N, stage_bytes, red);
+  const int NQ = N >> 2;
+  for (int e = threadIdx.x; e < BT * NQ; e += kStNT) {
+    const int b = e / NQ, o = 4 * (e - b * NQ);
+    epi(b, o, st_sum4(red, G, BT * N, b * N + o));
   }
   ptx::named_bar_sync(kStBarId, kStNT);
 }
@@ -763,17 +823,16 @@ StagedLayout staged_layout(const CellDims& d, int stages = 3) {
     o += (floats + 31) & ~31;  // 128-byte aligned buffers
     return at;
   };
-  y.xx = take(BT * 2 * d.R);
-  y.a = take(BT * 2 * d.D);
+  y.xx = take(2 * BT * 2 * d.R);  // two layer buffers
   y.z = take(BT * d.D);
   y.s = take(BT * d.S);
   y.hb = take(BT * d.H);
   y.lg = take(BT * d.A);
   y.red = take(kStNT * 4 * BT);
-  y.pops = take(3 * BT * d.R);
-  y.bias = take(3 * (2 * d.D + d.S + d.R));  // per-layer biases, prefetched with the pops
+  y.pops = take(4 * BT * d.R);
+  y.bias = take(4 * (2 * d.D + d.S + d.R));  // per-layer biases, prefetched with the pops
   y.hbias = take(d.H + d.A);
-  y.lcon = take(3 * d.L);                    // per-layer ring offsets (int64) and dilations
+  y.lcon = take(4 * d.L);                    // ring offsets (int64), slots of steps t, t+1
   y.cls = take(BT);
   y.bars = take(2 * 2 * kStStagesMax);
   y.ring = take(0);
@@ -784,30 +843,34 @@ StagedLayout staged_layout(const CellDims& d, int stages = 3) {
   return y;
 }
 
+// Per layer (gg = step * L + l, layer buffers xx[gg & 1] = x_l[t] | x_l[t-d]):
+//   push x_l[t] -> slot; dil partials; [bar] reduce + gate -> z, the pop of layer gg+1 into the
+//   other buffer, prefetch of layer gg+3; [bar] skip|res partials over z (one [D][S+R] weight
+//   matrix); [bar] s += .., x_{l+1} -> the other buffer; [bar]
 template <int BT>
 __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p, StagedLayout y) {
   extern __shared__ __align__(1024) float smf[];
   const CellDims d = p.d;
   const int R = d.R, D = d.D, S = d.S, H = d.H, A = d.A, L = d.L;
-  float* xx = smf + y.xx;  // [BT][2R]: x_l[t] | x_l[t-d]
-  float* a = smf + y.a;    // [BT][2D]
+  const int SR = S + R;
+  float* xx = smf + y.xx;  // [2][BT][2R]
   float* z = smf + y.z;    // [BT][D]
   float* s = smf + y.s;    // [BT][S]
   float* hb = smf + y.hb;  // [BT][H]
   float* lg = smf + y.lg;  // [BT][A]
   float* red = smf + y.red;
-  float* pops = smf + y.pops;  // [3][BT][R]: x_{t-d} of layers g, g+1, g+2
-  // [3][2D | S | R]: dil / skip / res biases of layers g, g+1, g+2 (global loads in the
+  float* pops = smf + y.pops;  // [4][BT][R]: prefetched x_{t-d} of layers gg % 4
+  // [4][2D | S | R]: dil / skip / res biases of the prefetched layers (global loads in the
   // epilogues would put an L2 round trip per GEMV on the chain)
   float* bias = smf + y.bias;
   float* hbias = smf + y.hbias;  // h1 | h2 biases
   int64_t* qoff_s = reinterpret_cast<int64_t*>(smf + y.lcon);
-  int* dil_s = reinterpret_cast<int*>(qoff_s + L);
-  const int NB = 2 * D + S + R;
+  int* slot_s = reinterpret_cast<int*>(qoff_s + L);  // [2][L]: slots of steps t, t+1
   int* cls = reinterpret_cast<int*>(smf + y.cls);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smf + y.bars);
   StageRing rg{bars, bars + kStStagesMax, smf + y.ring, y.stage_bytes / 4, 0, 0u,
                ptx::cluster_rank(), ptx::cluster_size(), y.stages};
+  const int NB = 2 * D + S + R;
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int s0 = blockIdx.x * BT;
@@ -815,6 +878,7 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
   const CellRun& run = p.run;
   const int B = p.B;
   const int sb = y.stage_bytes;
+  const int GL = run.n_steps * L;
   if (tid == 0) {
     for (int i = 0; i < rg.nst; ++i) {
       ptx::mbar_init(&rg.full[i], 1);
@@ -825,7 +889,8 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
   if (tid < BT) cls[tid] = (tid < nb) ? run.inputs[s0 + tid] : 0;
   for (int e = tid; e < L; e += blockDim.x) {
     qoff_s[e] = p.qoff[e];
-    dil_s[e] = p.dil[e];
+    slot_s[e] = (int)(run.t0 % p.dil[e]);
+    slot_s[L + e] = (int)((run.t0 + 1) % p.dil[e]);
   }
   for (int e = tid; e < H + A; e += blockDim.x) hbias[e] = e < H ? p.w.h1_b[e] : p.w.h2_b[e - H];
   if (rg.csize > 1) ptx::cluster_sync();  // every CTA's barriers exist before any multicast
@@ -837,8 +902,7 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
     for (int i = 0; i < run.n_steps; ++i) {
       for (int l = 0; l < L; ++l) {
         st_produce(rg, p.w.dilT + (size_t)l * 2 * R * 2 * D, 2 * R, 2 * D, sb, is);
-        st_produce(rg, p.w.skipT + (size_t)l * D * S, D, S, sb, is);
-        if (l + 1 < L) st_produce(rg, p.w.resT + (size_t)l * D * R, D, R, sb, is);
+        st_produce(rg, p.w.catT + (size_t)l * D * SR, D, SR, sb, is);
       }
       st_produce(rg, p.w.h1T, S, H, sb, is);
       st_produce(rg, p.w.h2T, H, A, sb, is);
@@ -849,26 +913,25 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
   }
 
   // ring pops: thread e owns (stream b, 4-channel chunk c4) for every layer -- it pushes the
-  // chunk and prefetches the same chunk of the layer two ahead
+  // chunk and prefetches the same chunk three layers ahead (program order covers slot reuse)
   const int Rp = (R + 3) & ~3;
   const int R4 = R >> 2;  // R % 4 == 0 here
   const size_t slot_elems = (size_t)((B + 127) / 128) * 128 * Rp;
-  const int G = run.n_steps * L;
-  auto slot_ptr = [&](int gg, int b, int c4) {
+  // layer gg of step i0 + (0 | 1): slot from the table of step t or t+1
+  auto slot_ptr = [&](int gg, int i0, int b, int c4) {
     const int l = gg % L;
-    const int64_t t = run.t0 + gg / L;
     const int st = s0 + b;
-    return p.queue + qoff_s[l] + (size_t)(t % dil_s[l]) * slot_elems +
+    return p.queue + qoff_s[l] + (size_t)slot_s[(gg / L - i0) * L + l] * slot_elems +
            ((size_t)((st >> 7) * (Rp / 4) + c4) * 128 + (st & 127)) * 4;
   };
-  auto prefetch = [&](int gg) {
-    if (gg < G) {
+  auto prefetch = [&](int gg, int i0) {
+    if (gg < GL) {
       for (int e = tid; e < nb * R4; e += kStNT) {
         const int b = e / R4, c4 = e % R4;
-        ptx::cp_async16(ptx::smem_u32(pops + ((gg % 3) * BT + b) * R + 4 * c4), slot_ptr(gg, b, c4));
+        ptx::cp_async16(ptx::smem_u32(pops + ((gg % 4) * BT + b) * R + 4 * c4), slot_ptr(gg, i0, b, c4));
       }
       const int l = gg % L;
-      float* bb = bias + (gg % 3) * NB;
+      float* bb = bias + (gg % 4) * NB;
       for (int e = tid; e < NB / 4; e += kStNT) {
         const int o = 4 * e;
         const float* src = o < 2 * D ? p.w.dil_b + (size_t)l * 2 * D + o
@@ -879,70 +942,100 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
     }
     ptx::cp_async_commit();
   };
-  prefetch(0);
-  prefetch(1);
+  auto take_pops = [&](int gg) {  // prefetched x_{t-d} of layer gg -> xx[gg & 1][.][R..2R)
+    float* xd = xx + (gg & 1) * BT * 2 * R + R;
+    for (int e = tid; e < nb * R4; e += kStNT) {
+      const int b = e / R4, c4 = e % R4;
+      *reinterpret_cast<float4*>(xd + b * 2 * R + 4 * c4) =
+          *reinterpret_cast<const float4*>(pops + ((gg % 4) * BT + b) * R + 4 * c4);
+    }
+  };
+  prefetch(0, 0);
+  prefetch(1, 0);
+  prefetch(2, 0);
+  ptx::cp_async_wait<2>();
+  take_pops(0);
 
   // measurement only (FW_SIMT_EXP=2): thread 0 of CTA 0 prints one layer's phase cycles
-  const bool trace = y.exp == 2 && blockIdx.x == 0 && tid == 0;
+  const bool trace = y.exp == 2 && blockIdx.x == 0 && (tid & 31) == 0;
   long long stamp[8];
   for (int i = 0; i < run.n_steps; ++i) {
     const int64_t t = run.t0 + i;
-    if (trace) stamp[7] = clock64();
+    float* x0 = xx + ((i * L) & 1) * BT * 2 * R;
     for (int e = tid; e < BT * R; e += kStNT) {
       const int b = e / R, r = e % R;
-      xx[b * 2 * R + r] = __ldg(p.w.embed + (size_t)cls[b] * R + r);
+      x0[b * 2 * R + r] = __ldg(p.w.embed + (size_t)cls[b] * R + r);
     }
     for (int e = tid; e < BT * S; e += kStNT) s[e] = 0.f;
+    if (i > 0)
+      for (int e = tid; e < L; e += kStNT) {  // slot tables of steps t, t+1
+        slot_s[e] = slot_s[L + e];
+        slot_s[L + e] = (int)((t + 1) % p.dil[e]);
+      }
     ptx::named_bar_sync(kStBarId, kStNT);
     for (int l = 0; l < L; ++l) {
       const int gg = i * L + l;
+      float* xc = xx + (gg & 1) * BT * 2 * R;
+      float* xn = xx + ((gg + 1) & 1) * BT * 2 * R;
+      const float* bl = bias + (gg % 4) * NB;  // (the prefetch of gg + 3 fills another)
       if (trace) stamp[0] = clock64();
-      // pop + push on slot t mod d_l (fast.py:131-147, 200-213): x_l[t-d] from the prefetch,
-      // x_l[t] into the slot
-      ptx::cp_async_wait<1>();
-      if (trace) stamp[1] = clock64();
+      // push x_l[t] into slot t mod d_l (fast.py:200-213; its pop, x_l[t-d], was read ahead)
       for (int e = tid; e < nb * R4; e += kStNT) {
         const int b = e / R4, c4 = e % R4;
-        const float4 old = *reinterpret_cast<const float4*>(pops + ((gg % 3) * BT + b) * R + 4 * c4);
-        *reinterpret_cast<float4*>(xx + b * 2 * R + R + 4 * c4) = old;
-        *reinterpret_cast<float4*>(slot_ptr(gg, b, c4)) =
-            *reinterpret_cast<const float4*>(xx + b * 2 * R + 4 * c4);
+        *reinterpret_cast<float4*>(slot_ptr(gg, i, b, c4)) =
+            *reinterpret_cast<const float4*>(xc + b * 2 * R + 4 * c4);
       }
-      prefetch(gg + 2);
+      if (trace) stamp[5] = clock64();
+      const int G1 = st_partial<BT>(rg, xc, 2 * R, 2 * R, 2 * D, sb, red);
+      if (trace) stamp[1] = clock64();
+      // gate: z = tanh(a[:D]) * sigmoid(a[D:]), a = partial sums + bias
+      for (int e = tid; e < BT * (D >> 1); e += kStNT) {
+        const int b = e / (D >> 1), j = 2 * (e - b * (D >> 1));
+        const int ea = b * 2 * D + j;
+        float2 va = *reinterpret_cast<const float2*>(red + ea);
+        float2 vs = *reinterpret_cast<const float2*>(red + ea + D);
+        for (int g = 1; g < G1; ++g) {
+          const float2 ua = *reinterpret_cast<const float2*>(red + (size_t)g * BT * 2 * D + ea);
+          const float2 us = *reinterpret_cast<const float2*>(red + (size_t)g * BT * 2 * D + ea + D);
+          va.x += ua.x, va.y += ua.y, vs.x += us.x, vs.y += us.y;
+        }
+        *reinterpret_cast<float2*>(z + b * D + j) =
+            make_float2(tanhf(va.x + bl[j]) * sigmoidf_(vs.x + bl[D + j]),
+                        tanhf(va.y + bl[j + 1]) * sigmoidf_(vs.y + bl[D + j + 1]));
+      }
+      ptx::cp_async_wait<1>();  // this thread's prefetch of layer gg + 1
+      if (gg + 1 < GL) take_pops(gg + 1);
+      prefetch(gg + 3, i);
+      if (trace) stamp[6] = clock64();
       ptx::named_bar_sync(kStBarId, kStNT);
       if (trace) stamp[2] = clock64();
-      const float* db = bias + (gg % 3) * NB;
-      st_gemv<BT>(rg, xx, 2 * R, 2 * R, 2 * D, sb, red,
-                  [&](int b, int o, float v) { a[b * 2 * D + o] = v + db[o]; });
+      const int G2 = st_partial<BT>(rg, z, D, D, SR, sb, red);
       if (trace) stamp[3] = clock64();
-      for (int e = tid; e < BT * D; e += kStNT) {
-        const int b = e / D, j = e % D;
-        z[e] = tanhf(a[b * 2 * D + j]) * sigmoidf_(a[b * 2 * D + D + j]);
+      const bool res = l + 1 < L;
+      for (int e = tid; e < BT * (SR >> 2); e += kStNT) {
+        const int b = e / (SR >> 2), o = 4 * (e - b * (SR >> 2));
+        const float4 v = add4(st_sum4(red, G2, BT * SR, b * SR + o), ST_C4(bl + 2 * D + o));
+        if (o < S) ST_F4(s + b * S + o) = add4(ST_F4(s + b * S + o), v);
+        else if (res) ST_F4(xn + b * 2 * R + (o - S)) = add4(ST_F4(xc + b * 2 * R + (o - S)), v);
       }
+      if (trace) stamp[7] = clock64();
       ptx::named_bar_sync(kStBarId, kStNT);
-      if (trace) stamp[4] = clock64();
-      const float* sbias = bias + (gg % 3) * NB + 2 * D;
-      st_gemv<BT>(rg, z, D, D, S, sb, red,
-                  [&](int b, int o, float v) { s[b * S + o] += v + sbias[o]; });
-      if (trace) stamp[5] = clock64();
-      if (l + 1 < L) {
-        const float* rb = bias + (gg % 3) * NB + 2 * D + S;
-        st_gemv<BT>(rg, z, D, D, R, sb, red,
-                    [&](int b, int o, float v) { xx[b * 2 * R + o] += v + rb[o]; });
+      if (trace) {
+        stamp[4] = clock64();
+        if (l == 5 && i == 3)
+          printf("staged trace l5 warp %d: push %lld dil %lld | gate work %lld bar %lld | skipres %lld | "
+                 "reduce work %lld bar %lld\n", warp, stamp[5] - stamp[0], stamp[1] - stamp[5],
+                 stamp[6] - stamp[1], stamp[2] - stamp[6], stamp[3] - stamp[2], stamp[7] - stamp[3],
+                 stamp[4] - stamp[7]);
       }
-      if (trace) stamp[6] = clock64();
-      if (trace && l == 5 && i == 3)
-        printf("staged trace l5: wait_pop %lld push %lld dil %lld gate %lld skip %lld res %lld\n",
-               stamp[1] - stamp[0], stamp[2] - stamp[1], stamp[3] - stamp[2], stamp[4] - stamp[3],
-               stamp[5] - stamp[4], stamp[6] - stamp[5]);
     }
     // head: logits = W2 relu(W1 relu(s) + b1) + b2
-    for (int e = tid; e < BT * S; e += kStNT) s[e] = fmaxf(s[e], 0.f);
+    for (int e = tid; e < BT * S / 4; e += kStNT) ST_F4(s + 4 * e) = relu4(ST_F4(s + 4 * e));
     ptx::named_bar_sync(kStBarId, kStNT);
     st_gemv<BT>(rg, s, S, S, H, sb, red,
-                [&](int b, int o, float v) { hb[b * H + o] = fmaxf(v + hbias[o], 0.f); });
+                [&](int b, int o, float4 v) { ST_F4(hb + b * H + o) = relu4(add4(v, ST_F4(hbias + o))); });
     st_gemv<BT>(rg, hb, H, H, A, sb, red,
-                [&](int b, int o, float v) { lg[b * A + o] = v + hbias[H + o]; });
+                [&](int b, int o, float4 v) { ST_F4(lg + b * A + o) = add4(v, ST_F4(hbias + H + o)); });
     if (run.logits != nullptr && i < run.n_logit_steps) {
       float* dst = run.logits + ((size_t)i * B + s0) * A;
       for (int e = tid; e < nb * A; e += kStNT) dst[e] = lg[e];
@@ -965,7 +1058,7 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
 bool staged_supported(const CellDims& d) {
   auto m4 = [](int v) { return v % 4 == 0; };
   return d.L >= 3 && m4(d.R) && m4(d.D) && m4(d.S) && m4(d.H) && m4(d.A) && 2 * d.D <= 1024 &&
-         d.S <= 1024 && d.H <= 1024 && d.A <= 1024 && d.R <= 1024 &&
+         d.S + d.R <= 1024 && d.H <= 1024 && d.A <= 1024 && d.R <= 1024 &&
          staged_layout<8>(d).stage_bytes >= 4 * 4 * 1024;
 }
 

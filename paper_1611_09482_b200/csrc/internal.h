@@ -68,6 +68,7 @@ struct SimtWeights {
   float* resT;   // [L][D][R]
   float* res_b;  // [L][R]
   float* skipT;  // [L][D][S]
+  float* catT;   // [L][D][S+R]: skipT | resT per row (the staged kernel's one z GEMV)
   float* skip_b; // [L][S]
   float* h1T;    // [S][H]
   float* h1_b;   // [H]
