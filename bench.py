@@ -132,9 +132,15 @@ def dominant_accounting(cell, batch, kernel):
     return f, b
 
 
-def traffic_per_launch(kernel):
+def simt_kernel_name(batch):
+    """The SIMT kernel the library selects (capi launch_cell_simt): one cluster per stream up
+    to 16 streams, else the weight-staged kernel."""
+    return "cell_cluster_kernel" if batch <= 16 else "cell_staged_kernel"
+
+
+def traffic_per_launch(kernel, batch):
     """DRAM bytes per step of the dominant kernel from the newest committed ncu summary."""
-    want = "step_kernel" if kernel == "tcgen05" else "cell_simt_kernel"
+    want = "step_kernel" if kernel == "tcgen05" else simt_kernel_name(batch)
     for f in sorted((ROOT / "profiles").glob("ncu_summary_*.json"), reverse=True):
         try:
             d = json.loads(f.read_text())
@@ -346,11 +352,12 @@ def main():
             roof = {"bound": "hbm", "achieved": k_bytes / k_s / 1e9, "peak": hbm / 1e9,
                     "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        traffic, tsrc = traffic_per_launch(kname)
+        traffic, tsrc = traffic_per_launch(kname, B)
         roof["traffic"] = traffic
         roof["kernel"] = ("step_kernel (persistent: chain + skip sum + heads + selection, one "
                           "cooperative launch per generate call, per-step share)" if kname == "tcgen05"
-                          else "cell_simt_kernel (one launch per generate call, per-step share)")
+                          else f"{simt_kernel_name(B)} (persistent fp32 SIMT kernel, one launch per "
+                          "generate call, per-step share)")
         roof["algorithmic_per_step"] = {"flop": k_flops, "bytes": k_bytes}
         roof["kernel_us_per_step"] = 1e6 * k_s
         roof["kernel_share_of_step"] = k_s / s_per_step
@@ -376,9 +383,11 @@ def main():
                        "layers": spec.cell.total_layers, "residual": spec.cell.residual_channels,
                        "skip": spec.cell.skip_channels, "kernel": kname,
                        "parallelism": f"streams sharded x{world}",
-                       "l2": f"queues {gen.queue_bytes / 1e9:.1f} GB >> L2 (126 MB); each step "
-                             f"touches {qbytes / 1e6:.0f} MB of fresh queue slots (no flush "
-                             "needed)"},
+                       "l2": (f"queues {gen.queue_bytes / 1e9:.1f} GB >> L2 (126 MB); each step "
+                              f"touches {qbytes / 1e6:.0f} MB of fresh queue slots (no flush "
+                              "needed)") if gen.queue_bytes > 126e6 else
+                             (f"queues {gen.queue_bytes / 1e6:.0f} MB fit in L2: steady-state "
+                              "generation keeps them resident, as a deployment would (no flush)")},
             "roofline": roof,
             "e2e": {"value": total_batch * args.steps / e2e_s, "unit": "samples/s",
                     "h2d_bytes_per_step": B * 4 / args.steps, "d2h_bytes_per_step": B * 4,
