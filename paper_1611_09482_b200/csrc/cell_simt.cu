@@ -601,7 +601,7 @@ cudaError_t launch_cluster(const SimtParams& p, cudaStream_t st) {
 // The ring pops are prefetched two layers ahead by the threads that push the same elements
 // (cp.async: program order covers the slot reuse, as in the tcgen05 chain). Same cell, same
 // pop -> compute -> push order per layer as cell_simt_kernel (fast.py:131-213).
-constexpr int kStNT = 256;                 // compute threads (8 warps)
+constexpr int kStNT = 256;                 // compute threads (8 warps; 16 measured slower: 908 vs 721 us/step on cfg5)
 constexpr int kStThreads = kStNT + 32;     // + the weight producer warp
 constexpr int kStStagesMax = 8;            // weight ring depth (runtime, <= 8)
 constexpr int kStBarId = 1;                // named barrier of the compute warps

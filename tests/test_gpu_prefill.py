@@ -194,3 +194,20 @@ def test_naive_generation_equals_fast(cuda, models):
     b = cell_fast_generate(model, primer, 60, kernel="simt")
     assert a.shape == b.shape == (1, 60)
     assert np.array_equal(a, b)
+
+
+def test_prefill_then_staged_kernel_continues(cuda, models):
+    """21 streams run on the weight-staged SIMT kernel: queues filled by the prefill (same fp32
+    slot layout) and continued by the kernel give the logits of an all-stepped run and the
+    oracle's teacher-forced forward."""
+    B = 21
+    x = teacher(140, B, 9)
+    _, ref = stepped(models["simt"], "simt", B, x)
+    gen = CellGenerator(models["simt"], B, kernel="simt")
+    gen.prefill(torch.as_tensor(x[:100], device="cuda"))
+    _, lg = gen.generate(torch.as_tensor(x[100:], device="cuda"), 40, Sampler(0), n_logit_steps=40)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(lg.cpu().numpy() - ref[100:])) <= 1e-4
+    o = oc.CellOracle(models["simt"])
+    for b in (0, 20):
+        assert np.max(np.abs(ref[:, b] - o.forward_full(x[:, b]))) <= 1e-4
