@@ -44,7 +44,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     tmp = PKG / "build"
     tmp.mkdir(exist_ok=True)
     flags = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-             "-I", str(ROOT / "include"), *ARCH]
+             "-I", str(ROOT / "include"), *ARCH, *os.environ.get("FW_NVCC_EXTRA", "").split()]
     procs = []
     for src in SOURCES:
         obj = tmp / (Path(src).stem + ".o")

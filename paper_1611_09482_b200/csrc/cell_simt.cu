@@ -610,7 +610,6 @@ struct StagedLayout {
   int stage_bytes;  // one weight stage
   int issuers;      // producer lanes issuing a chunk's bulk copies
   int stages;       // ring depth
-  int exp;          // measurement only: 1 = the producer skips the weight copies
   // float offsets of the activation buffers from the start of dynamic smem
   int xx, z, s, hb, lg, red, pops, bias, hbias, lcon, cls, ring, bars;
   size_t total;
@@ -629,7 +628,6 @@ struct StageRing {
   int stage_floats;
   int slot;
   uint32_t ph;
-  uint32_t crank, csize;  // cluster rank / size: each CTA loads 1/csize of a stage, multicast
   int nst;                // stages in the ring
   __device__ __forceinline__ void advance() {
     if (++slot == nst) {
@@ -641,8 +639,8 @@ struct StageRing {
 
 // Producer side of one GEMV: its K-chunks into the ring, run by the whole producer warp.
 // A chunk is split into `issuers` bulk copies issued by different lanes (one thread's bulk
-// copies execute one after another); with a cluster each CTA loads 1/csize of every slice and
-// multicasts it to the cluster.
+// copies execute one after another). (TMA multicast of each stage across a 2/4/8-CTA cluster
+// was measured slower, DESIGN.md section 4 K1s.)
 __device__ __forceinline__ void st_produce(StageRing& rg, const float* W, int K, int N,
                                            int stage_bytes, int issuers) {
   const int lane = threadIdx.x & 31;
@@ -651,31 +649,16 @@ __device__ __forceinline__ void st_produce(StageRing& rg, const float* W, int K,
     const int rows = min(kc, K - k0);
     const uint32_t bytes = (uint32_t)rows * N * 4;
     if (lane == 0) {
-      // the slot is free once every compute warp of every CTA of the cluster released it
-      if (rg.csize == 1) ptx::mbar_wait(&rg.empty[rg.slot], rg.ph ^ 1u);
-      else ptx::mbar_wait_cluster(&rg.empty[rg.slot], rg.ph ^ 1u);
-      if (issuers == 0) ptx::mbar_arrive(&rg.full[rg.slot]);
-      else ptx::mbar_arrive_expect_tx(&rg.full[rg.slot], bytes);
+      ptx::mbar_wait(&rg.empty[rg.slot], rg.ph ^ 1u);  // every compute warp released it
+      ptx::mbar_arrive_expect_tx(&rg.full[rg.slot], bytes);
     }
     __syncwarp();
-    const uint32_t parts = rg.csize * (uint32_t)max(issuers, 1);
-    const uint32_t slice = (bytes + 16 * parts - 1) / (16 * parts) * 16;
-    const uint32_t off = (rg.crank * (uint32_t)issuers + (uint32_t)lane) * slice;
-    if (lane < issuers && off < bytes) {  // (issuers == 0: measurement, no copies)
-      const uint32_t n = min(slice, bytes - off);
-      uint8_t* dst = reinterpret_cast<uint8_t*>(rg.buf + (size_t)rg.slot * rg.stage_floats) + off;
-      const uint8_t* src = reinterpret_cast<const uint8_t*>(W + (size_t)k0 * N) + off;
-      if (rg.csize == 1) {
-        ptx::bulk_g2s(dst, src, n, &rg.full[rg.slot]);
-      } else {
-        const uint16_t mask = (uint16_t)((1u << rg.csize) - 1u);
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-            " [%0], [%1], %2, [%3], %4;" ::"r"(ptx::smem_u32(dst)),
-            "l"(src), "r"(n), "r"(ptx::smem_u32(&rg.full[rg.slot])), "h"(mask)
-            : "memory");
-      }
-    }
+    const uint32_t slice = (bytes + 16 * issuers - 1) / (16 * issuers) * 16;
+    const uint32_t off = (uint32_t)lane * slice;
+    if (lane < issuers && off < bytes)
+      ptx::bulk_g2s(reinterpret_cast<uint8_t*>(rg.buf + (size_t)rg.slot * rg.stage_floats) + off,
+                    reinterpret_cast<const uint8_t*>(W + (size_t)k0 * N) + off,
+                    min(slice, bytes - off), &rg.full[rg.slot]);
     rg.advance();
   }
 }
@@ -730,14 +713,9 @@ __device__ __forceinline__ int st_partial_ob(StageRing& rg, const float* in, int
         }
       }
       if (qq == tid) {
-        // (a cluster-scope release waits for the warp's outstanding global stores: without a
-        // cluster the CTA-scope arrive keeps the ring pushes off the chain)
+        // (CTA-scope release: a cluster-scope one would wait for the ring-push stores)
         __syncwarp();
-        if (rg.csize == 1) {
-          if (lane == 0) ptx::mbar_arrive(&rg.empty[rg.slot]);
-        } else if (lane < (int)rg.csize) {
-          ptx::mbar_arrive_remote(ptx::mapa(&rg.empty[rg.slot], (uint32_t)lane));
-        }
+        if (lane == 0) ptx::mbar_arrive(&rg.empty[rg.slot]);
         rg.advance();
       }
     }
@@ -755,11 +733,7 @@ __device__ __forceinline__ int st_partial_ob(StageRing& rg, const float* in, int
     for (int k0 = 0; k0 < K; k0 += kc) {
       ptx::mbar_wait(&rg.full[rg.slot], rg.ph);
       __syncwarp();
-      if (rg.csize == 1) {
-        if (lane == 0) ptx::mbar_arrive(&rg.empty[rg.slot]);
-      } else if (lane < (int)rg.csize) {
-        ptx::mbar_arrive_remote(ptx::mapa(&rg.empty[rg.slot], (uint32_t)lane));
-      }
+      if (lane == 0) ptx::mbar_arrive(&rg.empty[rg.slot]);
       rg.advance();
     }
   }
@@ -869,7 +843,7 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
   int* cls = reinterpret_cast<int*>(smf + y.cls);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smf + y.bars);
   StageRing rg{bars, bars + kStStagesMax, smf + y.ring, y.stage_bytes / 4, 0, 0u,
-               ptx::cluster_rank(), ptx::cluster_size(), y.stages};
+               y.stages};
   const int NB = 2 * D + S + R;
 
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -882,7 +856,7 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
   if (tid == 0) {
     for (int i = 0; i < rg.nst; ++i) {
       ptx::mbar_init(&rg.full[i], 1);
-      ptx::mbar_init(&rg.empty[i], kStNT / 32 * rg.csize);
+      ptx::mbar_init(&rg.empty[i], kStNT / 32);
     }
     ptx::fence_mbar_init();
   }
@@ -893,12 +867,11 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
     slot_s[L + e] = (int)((run.t0 + 1) % p.dil[e]);
   }
   for (int e = tid; e < H + A; e += blockDim.x) hbias[e] = e < H ? p.w.h1_b[e] : p.w.h2_b[e - H];
-  if (rg.csize > 1) ptx::cluster_sync();  // every CTA's barriers exist before any multicast
-  else __syncthreads();
+  __syncthreads();
 
   if (warp == kStNT / 32) {
     // ---- weight producer: the step's GEMVs in the compute warps' order ----
-    const int is = y.exp == 1 ? 0 : y.issuers;
+    const int is = y.issuers;
     for (int i = 0; i < run.n_steps; ++i) {
       for (int l = 0; l < L; ++l) {
         st_produce(rg, p.w.dilT + (size_t)l * 2 * R * 2 * D, 2 * R, 2 * D, sb, is);
@@ -907,8 +880,6 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
       st_produce(rg, p.w.h1T, S, H, sb, is);
       st_produce(rg, p.w.h2T, H, A, sb, is);
     }
-    __syncwarp();
-    if (rg.csize > 1) ptx::cluster_sync();  // the peers' multicasts and arrivals are done
     return;
   }
 
@@ -956,9 +927,6 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
   ptx::cp_async_wait<2>();
   take_pops(0);
 
-  // measurement only (FW_SIMT_EXP=2): thread 0 of CTA 0 prints one layer's phase cycles
-  const bool trace = y.exp == 2 && blockIdx.x == 0 && (tid & 31) == 0;
-  long long stamp[8];
   for (int i = 0; i < run.n_steps; ++i) {
     const int64_t t = run.t0 + i;
     float* x0 = xx + ((i * L) & 1) * BT * 2 * R;
@@ -978,16 +946,13 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
       float* xc = xx + (gg & 1) * BT * 2 * R;
       float* xn = xx + ((gg + 1) & 1) * BT * 2 * R;
       const float* bl = bias + (gg % 4) * NB;  // (the prefetch of gg + 3 fills another)
-      if (trace) stamp[0] = clock64();
       // push x_l[t] into slot t mod d_l (fast.py:200-213; its pop, x_l[t-d], was read ahead)
       for (int e = tid; e < nb * R4; e += kStNT) {
         const int b = e / R4, c4 = e % R4;
         *reinterpret_cast<float4*>(slot_ptr(gg, i, b, c4)) =
             *reinterpret_cast<const float4*>(xc + b * 2 * R + 4 * c4);
       }
-      if (trace) stamp[5] = clock64();
       const int G1 = st_partial<BT>(rg, xc, 2 * R, 2 * R, 2 * D, sb, red);
-      if (trace) stamp[1] = clock64();
       // gate: z = tanh(a[:D]) * sigmoid(a[D:]), a = partial sums + bias
       for (int e = tid; e < BT * (D >> 1); e += kStNT) {
         const int b = e / (D >> 1), j = 2 * (e - b * (D >> 1));
@@ -1006,11 +971,8 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
       ptx::cp_async_wait<1>();  // this thread's prefetch of layer gg + 1
       if (gg + 1 < GL) take_pops(gg + 1);
       prefetch(gg + 3, i);
-      if (trace) stamp[6] = clock64();
       ptx::named_bar_sync(kStBarId, kStNT);
-      if (trace) stamp[2] = clock64();
       const int G2 = st_partial<BT>(rg, z, D, D, SR, sb, red);
-      if (trace) stamp[3] = clock64();
       const bool res = l + 1 < L;
       for (int e = tid; e < BT * (SR >> 2); e += kStNT) {
         const int b = e / (SR >> 2), o = 4 * (e - b * (SR >> 2));
@@ -1018,16 +980,7 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
         if (o < S) ST_F4(s + b * S + o) = add4(ST_F4(s + b * S + o), v);
         else if (res) ST_F4(xn + b * 2 * R + (o - S)) = add4(ST_F4(xc + b * 2 * R + (o - S)), v);
       }
-      if (trace) stamp[7] = clock64();
       ptx::named_bar_sync(kStBarId, kStNT);
-      if (trace) {
-        stamp[4] = clock64();
-        if (l == 5 && i == 3)
-          printf("staged trace l5 warp %d: push %lld dil %lld | gate work %lld bar %lld | skipres %lld | "
-                 "reduce work %lld bar %lld\n", warp, stamp[5] - stamp[0], stamp[1] - stamp[5],
-                 stamp[6] - stamp[1], stamp[2] - stamp[6], stamp[3] - stamp[2], stamp[7] - stamp[3],
-                 stamp[4] - stamp[7]);
-      }
     }
     // head: logits = W2 relu(W1 relu(s) + b1) + b2
     for (int e = tid; e < BT * S / 4; e += kStNT) ST_F4(s + 4 * e) = relu4(ST_F4(s + 4 * e));
@@ -1052,7 +1005,6 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
     ptx::named_bar_sync(kStBarId, kStNT);
   }
   ptx::cp_async_wait<0>();
-  if (rg.csize > 1) ptx::cluster_sync();
 }
 
 bool staged_supported(const CellDims& d) {
@@ -1069,34 +1021,13 @@ cudaError_t launch_staged(const SimtParams& p, cudaStream_t st) {
   StagedLayout y = staged_layout<BT>(p.d, stages);
   if (y.stage_bytes < 4 * 4 * 1024) y = staged_layout<BT>(p.d, 3);
   y.issuers = 4;
-  if (const char* ev = getenv("FW_SIMT_EXP")) y.exp = atoi(ev);
   if (const char* ev = getenv("FW_SIMT_ISSUERS")) y.issuers = max(1, min(32, atoi(ev)));
   cudaError_t e = cudaFuncSetAttribute(cell_staged_kernel<BT>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)y.total);
   if (e != cudaSuccess) return e;
-  // clusters of C CTAs share each weight stage (multicast): L2 serves 1/C of the bytes
-  int C = 1;
-  if (const char* ev = getenv("FW_SIMT_MCAST")) C = atoi(ev);
-  if (C != 1 && C != 2 && C != 4 && C != 8) C = 1;
-  const int grid = ((p.B + BT - 1) / BT + C - 1) / C * C;
-  if (C == 1) {
-    cell_staged_kernel<BT><<<grid, kStThreads, y.total, st>>>(p, y);
-    return cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(kStThreads);
-  cfg.dynamicSmemBytes = y.total;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = C;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  void* args[] = {const_cast<SimtParams*>(&p), const_cast<StagedLayout*>(&y)};
-  return cudaLaunchKernelExC(&cfg, (const void*)cell_staged_kernel<BT>, args);
+  const int grid = (p.B + BT - 1) / BT;
+  cell_staged_kernel<BT><<<grid, kStThreads, y.total, st>>>(p, y);
+  return cudaGetLastError();
 }
 
 constexpr size_t kPrePopMax = 64 * 1024;  // bytes of smem the pre-pop buffer may take

@@ -19,8 +19,7 @@ def main():
     bts = os.environ.get("BTS", "1,2,4,8").split(",")
     variants = [(f"staged_bt{b}", "1", b) for b in bts if b] + \
         ([("ldg", "0", None)] if os.environ.get("LDG", "1") == "1" else [])
-    mc = "mc%s_is%s_st%s" % (os.environ.get("FW_SIMT_MCAST", "1"), os.environ.get("FW_SIMT_ISSUERS", "4"),
-                            os.environ.get("FW_SIMT_STAGES", "3"))
+    mc = "is%s_st%s" % (os.environ.get("FW_SIMT_ISSUERS", "4"), os.environ.get("FW_SIMT_STAGES", "3"))
     for name, staged, bt in variants:
         name = f"{name}_{mc}" if staged == "1" else name
         os.environ["FW_SIMT_STAGED"] = staged
