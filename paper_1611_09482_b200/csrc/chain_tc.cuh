@@ -579,18 +579,20 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
         trace_g(a, t2, 24);
         tc_fence_before();
         named_bar_sync(1, 256);
-        if (i + 1 < a.n_steps) init_acc();
-        trace_g(a, t2, 25);
+        // hand the classes to the chain first: the next step's skip accumulator (init_acc,
+        // global bias loads + TMEM stores) is not needed before its layer 0 publishes z
         if (warp == 2 && lane == 0) {
           red_release_gpu(a.cls_ready + p, 1u);
           trace_g(a, k == 0, 6);
           if (i == a.n_steps - 2) trace_g(a, k == 0, 17);
         }
+        if (i + 1 < a.n_steps) init_acc();
+        trace_g(a, t2, 25);
       } else {
         own_half(hbias);  // h columns 256..511 into this image's chunks 4..7
-        if (i + 1 < a.n_steps) init_acc();
         mbar_wait_cluster(a_free, (uint32_t)i & 1);
-        send_half();
+        send_half();  // (before init_acc: block 0's head2 waits for this half of h)
+        if (i + 1 < a.n_steps) init_acc();
       }
     }
   } else if (warp >= 10 && warp < 14) {
