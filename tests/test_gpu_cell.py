@@ -340,10 +340,12 @@ def test_staged_simt_kernel_matches_oracle_and_ldg_kernel(cuda, monkeypatch, bt)
             ref = o.forward_full(cls[:, b])
             assert np.max(np.abs(lg[:, b] - ref)) <= 1e-4, (bt, B, b)
         primer = cls[:3]
-        s = Sampler(configs.SAMPLE_GUMBEL, 11)
-        got, _ = run(CellGenerator(m, B, kernel="simt"), primer, 40, s, 0)
-        monkeypatch.setenv("FW_SIMT_STAGED", "0")
-        monkeypatch.delenv("FW_SIMT_BT")
-        want, _ = run(CellGenerator(m, B, kernel="simt"), primer, 40, s, 0)
-        monkeypatch.setenv("FW_SIMT_BT", bt)
-        assert (got != want).mean() < 0.02  # near-ties may flip a class, not the run
+        for mode in (configs.SAMPLE_GUMBEL, configs.SAMPLE_INVCDF):
+            s = Sampler(mode, 11)
+            monkeypatch.setenv("FW_SIMT_STAGED", "1")
+            got, _ = run(CellGenerator(m, B, kernel="simt"), primer, 40, s, 0)
+            monkeypatch.setenv("FW_SIMT_STAGED", "0")
+            monkeypatch.delenv("FW_SIMT_BT")
+            want, _ = run(CellGenerator(m, B, kernel="simt"), primer, 40, s, 0)
+            monkeypatch.setenv("FW_SIMT_BT", bt)
+            assert (got != want).mean() < 0.02, mode  # near-ties may flip a class, not the run
