@@ -259,7 +259,8 @@ __device__ __forceinline__ void epi_relu_image_smem(uint32_t trow, int r, int c0
 // hold bias + noise (Gumbel) or the bias alone (other modes), so no bias loads are needed.
 __device__ __forceinline__ void epi_select(uint32_t trow, int r, int h, int stream,
                                         const SelectArgs& g, float* xch, int noise_col = -1,
-                                        bool add_has_bias = false, const ChainArgs* tra = nullptr) {
+                                        bool add_has_bias = false, const ChainArgs* tra = nullptr,
+                                        bool folded = false) {
   const int HALF = g.A / 2, A = g.A, mode = g.mode;
   const float* bias = g.bias;
   const uint32_t prefix = noise_prefix(g.seed, (uint32_t)(g.stream_offset + stream), (uint32_t)g.t);
@@ -269,7 +270,32 @@ __device__ __forceinline__ void epi_select(uint32_t trow, int r, int h, int stre
   const bool pre_noise = noise_col >= 0 && mode == FW_SAMPLE_GUMBEL;
   float best = -INFINITY, mx = -INFINITY;
   int bi = A;
-  if (tm_add) {
+  if (folded) {
+    // head2 accumulated onto (bias + noise) in TMEM columns noise_col..: the scores are
+    // there already (argmax / Gumbel steps without logits output)
+#pragma unroll 1
+    for (int cc = 0; cc < HALF / 64; ++cc) {
+      float x[64];
+      tmem_ld64(trow + noise_col + cbase + 64 * cc, x);
+      float bv[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      int bj[4] = {0, 1, 2, 3};
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        if (x[i] > bv[i & 3]) {
+          bv[i & 3] = x[i];
+          bj[i & 3] = i;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int col = cbase + 64 * cc + bj[u];
+        if (bv[u] > best || (bv[u] == best && col < bi)) {
+          best = bv[u];
+          bi = col;
+        }
+      }
+    }
+  } else if (tm_add) {
     // x = acc + (bias + noise): the score (Gumbel) or the logit (other modes), one pass with
     // no memory traffic. Four independent running maxima (a single compare-select chain is
     // latency-bound), merged lowest index first on ties; mx (inverse CDF) is the max logit.

@@ -357,6 +357,11 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
 // own A image and bulk-copies it into the peer's; both run head1 (256 columns of h each)
 // with A resident and only W1 streamed; block 1 sends its half of h into block 0's image
 // once block 0's head1 has released it; block 0 runs head2 and the selection rule.
+// Step i's head2 accumulates onto the selection's bias (+ noise) columns: every step that
+// writes no logits, except under the inverse-CDF rule (it needs the logits themselves).
+__device__ __forceinline__ bool pair_folds(const ChainArgs& a, int i) {
+  return a.sel.mode != FW_SAMPLE_INVCDF && !(a.sel.logits_base != nullptr && i < a.sel.n_logit_steps);
+}
 __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem, int k) {
   const int p = k >> 1, e = k & 1;  // e == cluster rank
   const int L = a.L, S = a.S, H = a.H;
@@ -476,13 +481,18 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
       trace_g(a, k == 0 && lane == 0, 7);
       for (int g = 0; g < (sel_block ? 2 : 1); ++g) {
         // K order: own half of the image first (its chunks are written here), the peer's
-        // half (arriving through DSMEM) second -- the MMAs start before the exchange ends
+        // half (arriving through DSMEM) second -- the MMAs start before the exchange ends.
+        // head2 of a step without logits output accumulates onto the bias (+ Gumbel noise)
+        // the noise warps left in TMEM [256,512): the selection reads finished scores.
+        const bool fold = g == 1 && pair_folds(a, i);
+        const uint32_t dacc = fold ? tmem + 256 : tmem;
         const int j0 = g == 0 ? 0 : ks, nj = g == 0 ? ks : kh;
         for (int j = j0; j < j0 + nj; ++j) {
           const int J = i * nw + j, st = J % kWStages;
           const int c = chunk_of(j), jj = j - j0;
           if (jj == 0) {
             mbar_wait(own_ready, (uint32_t)(2 * i + g) & 1);  // (+ previous accumulator read)
+            if (fold) mbar_wait(noise_ready, (uint32_t)i & 1);
             tc_fence_after();
             trace_g(a, k == 0 && lane == 0, 8 + 3 * g);
           }
@@ -498,8 +508,8 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              mma_bf16(tmem, sdesc_sw128(si + c * kTile + kk * 32),
-                       sdesc_sw128(sw + st * kWStage + kk * 32), id, (jj | kk) ? 1u : 0u);
+              mma_bf16(dacc, sdesc_sw128(si + c * kTile + kk * 32),
+                       sdesc_sw128(sw + st * kWStage + kk * 32), id, (fold || jj || kk) ? 1u : 0u);
             mma_commit(wempty + st);
           }
           __syncwarp();
@@ -575,7 +585,8 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
         trace_g(a, k == 0 && warp == 2 && lane == 0, 5);
         const SelectArgs sel = sel_step(a.sel, a.t0, i);
         trace_g(a, t2, 28);
-        epi_select(trow, r, hf, p * 128 + r, sel, xch, 256, true, t2 ? &a : nullptr);
+        epi_select(trow, r, hf, p * 128 + r, sel, xch, 256, true, t2 ? &a : nullptr,
+                   pair_folds(a, i));
         trace_g(a, t2, 24);
         tc_fence_before();
         named_bar_sync(1, 256);

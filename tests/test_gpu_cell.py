@@ -349,3 +349,20 @@ def test_staged_simt_kernel_matches_oracle_and_ldg_kernel(cuda, monkeypatch, bt)
             want, _ = run(CellGenerator(m, B, kernel="simt"), primer, 40, s, 0)
             monkeypatch.setenv("FW_SIMT_BT", bt)
             assert (got != want).mean() < 0.02, mode  # near-ties may flip a class, not the run
+
+
+@pytest.mark.parametrize("sampler", [configs.SAMPLE_GUMBEL, configs.SAMPLE_ARGMAX])
+def test_tcgen05_pair_tail_scores_folded_into_head2(cuda, sampler):
+    """Pair-mode steps without logits output accumulate head2 onto the bias (+ Gumbel noise)
+    in TMEM and select from those scores; steps with logits keep them separate. Both give
+    the same classes (up to near-ties), and the logits run matches the oracle."""
+    cfg = CellConfig(1, 4, 128, 128, 512, weight_dtype="bf16", bias="fan_in", init_seed=8)
+    m = build_cell_model(cfg)
+    B, n = 256, 24
+    primer = np.random.default_rng(3).integers(0, 256, (2, B))
+    s = Sampler(sampler, 21)
+    folded, _ = run(CellGenerator(m, B, kernel="tcgen05"), primer, n, s, 0)
+    plain, lg = run(CellGenerator(m, B, kernel="tcgen05"), primer, n, s, n)
+    assert (folded != plain).mean() < 0.01
+    check_streams(oc.CellOracle(m, exact=False), primer, plain, lg, [0, 200], sampler, 21,
+                  *TOL["bf16"])
