@@ -1085,7 +1085,7 @@ cudaError_t launch_cell_simt(const Handle& h, const CellRun& run, cudaStream_t s
   const char* se = getenv("FW_SIMT_STAGED");
   if (staged_supported(h.dims) && !(se != nullptr && atoi(se) == 0)) {
     int bt = 8;
-    for (int c : {1, 2, 4, 8})
+    for (int c : {1, 2, 4, 6, 7, 8})
       if ((B + c - 1) / c <= 148) {
         bt = c;
         break;
@@ -1095,6 +1095,8 @@ cudaError_t launch_cell_simt(const Handle& h, const CellRun& run, cudaStream_t s
       case 1: return launch_staged<1>(p, st);
       case 2: return launch_staged<2>(p, st);
       case 4: return launch_staged<4>(p, st);
+      case 6: return launch_staged<6>(p, st);
+      case 7: return launch_staged<7>(p, st);
       default: return launch_staged<8>(p, st);
     }
   }

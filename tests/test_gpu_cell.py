@@ -321,7 +321,7 @@ def test_tcgen05_padded_batch(cuda, B):
     assert gen.step_index == 6
 
 
-@pytest.mark.parametrize("bt", ["1", "2", "4", "8"])
+@pytest.mark.parametrize("bt", ["1", "2", "4", "7", "8"])
 def test_staged_simt_kernel_matches_oracle_and_ldg_kernel(cuda, monkeypatch, bt):
     """The weight-staged fp32 kernel (bulk-copied weight ring, FW_SIMT_BT streams per CTA, the
     last CTA partly filled) gives the oracle's teacher-forced logits, including shapes whose
