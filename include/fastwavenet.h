@@ -91,7 +91,11 @@ typedef struct fw_sampler {
 
 /* = init_state (fast.py:122-128) for `batch` independent streams: uploads and
  * repacks the weights, allocates the per-layer ring queues
- * (sum_l d_l * batch * R floats, fp32) in HBM and zero-fills them. */
+ * in HBM and zero-fills them: sum_l d_l * batch * R values, fp32 on the SIMT path and
+ * fp16 on the tcgen05 path (the slot holds the MMA operand the tensor cores consume; every
+ * pop would round to it anyway, so results are identical). Class ids outside [0, A) are
+ * rejected by the host entry points and the Python shim; on the device they are clamped
+ * into range (never read out of bounds). */
 int fw_cell_create(const fw_cell_desc* desc, int32_t batch, int32_t device, int32_t kernel,
                    fw_handle** out);
 
@@ -132,6 +136,14 @@ int fw_cell_generate_host(fw_handle* h, const int32_t* h_inputs, int32_t n_input
  * forces either). */
 int fw_cell_prefill(fw_handle* h, const int32_t* d_inputs, int32_t T, float* d_logits,
                     void* stream);
+
+/* The selection rule alone (the step kernels' final stage) over rows of
+ * logits: row i of d_logits [n_rows][A] is stream i % B (global id stream_offset + i % B)
+ * at step `step + i / B`, with the same counter-hash noise as the step kernels; the chosen
+ * class goes to d_out[i]. The cache-free generator (naive.py:113-131's feedback rule on
+ * the recomputed logits) selects through this. */
+int fw_cell_select(fw_handle* h, const float* d_logits, int64_t n_rows, int64_t step,
+                   const fw_sampler* sampler, int32_t* d_out, void* stream);
 
 /* ---- plain mode: the reference's own stack, float64 (model.py, fast.py) ---- */
 

@@ -18,7 +18,7 @@ FW_KERNEL_AUTO, FW_KERNEL_SIMT, FW_KERNEL_TCGEN05 = 0, 1, 2
 # Every symbol include/fastwavenet.h declares (checked by tests/test_capi_symbols.py).
 EXPORTS = (
     "fw_cell_create", "fw_cell_step", "fw_cell_generate", "fw_cell_generate_host",
-    "fw_cell_prefill", "fw_plain_create", "fw_plain_naive", "fw_plain_step", "fw_plain_generate", "fw_plain_pop",
+    "fw_cell_prefill", "fw_cell_select", "fw_plain_create", "fw_plain_naive", "fw_plain_step", "fw_plain_generate", "fw_plain_pop",
     "fw_plain_compute", "fw_plain_push", "fw_reset", "fw_step_index", "fw_queue_bytes",
     "fw_kernel_kind", "fw_last_launch_count", "fw_destroy", "fw_last_error", "fw_version",
     "fw_debug_trace", "fw_debug_copy", "fw_debug_timing", "fw_debug_timing_read",
@@ -79,6 +79,7 @@ def load(path: Path | None = None) -> C.CDLL:
         "fw_cell_generate_host": (C.c_int, [H, P, C.c_int32, C.c_int32, P,
                                             C.POINTER(FwSampler), P]),
         "fw_cell_prefill": (C.c_int, [H, P, C.c_int32, P, P]),
+        "fw_cell_select": (C.c_int, [H, P, C.c_int64, C.c_int64, C.POINTER(FwSampler), P, P]),
         "fw_plain_create": (C.c_int, [C.POINTER(FwPlainDesc), C.c_int32, C.c_int32, C.POINTER(H)]),
         "fw_plain_step": (C.c_int, [H, P, P, P]),
         "fw_plain_naive": (C.c_int, [H, P, C.c_int32, P, P]),

@@ -60,7 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed: {' '.join(cmd)}")
     tmp_lib = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), "-shared", "-o", str(tmp_lib), *map(str, objs), *ARCH, "-ldl"]
+    cmd = [nvcc(), "-shared", "-o", str(tmp_lib), *map(str, objs), *ARCH]
     subprocess.run(cmd, check=True)
     os.replace(tmp_lib, LIB)
     return LIB

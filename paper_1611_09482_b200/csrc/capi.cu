@@ -409,6 +409,8 @@ int fw_cell_generate_host(fw_handle* fh, const int32_t* h_inputs, int32_t n_inpu
   if (n_steps == 0) return FW_OK;
   if (n_inputs < 1 || !h_inputs || !h_out) return invalid("null host buffer or no inputs");
   Handle& h = fh->h;
+  for (int64_t i = 0, n = (int64_t)n_inputs * h.user_batch; i < n; ++i)
+    if (h_inputs[i] < 0 || h_inputs[i] >= h.dims.A) return invalid("input class ids out of range");
   FW_CUDA(cudaSetDevice(h.device));
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int64_t need = ((int64_t)n_inputs + n_steps) * h.user_batch;
@@ -429,6 +431,22 @@ int fw_cell_generate_host(fw_handle* fh, const int32_t* h_inputs, int32_t n_inpu
   FW_CUDA(cudaMemcpyAsync(h_out, d_out, sizeof(int32_t) * (size_t)n_steps * h.user_batch,
                           cudaMemcpyDeviceToHost, st));
   FW_CUDA(cudaStreamSynchronize(st));
+  return FW_OK;
+}
+
+int fw_cell_select(fw_handle* fh, const float* d_logits, int64_t n_rows, int64_t step,
+                   const fw_sampler* sampler, int32_t* d_out, void* stream) {
+  int rc = check_handle(fh, false);
+  if (rc) return rc;
+  if ((rc = validate_sampler(sampler))) return rc;
+  if (n_rows < 0) return invalid("n_rows must be non-negative");
+  if (n_rows == 0) return FW_OK;
+  if (!d_logits || !d_out) return invalid("d_logits and d_out must not be null");
+  Handle& h = fh->h;
+  FW_CUDA(cudaSetDevice(h.device));
+  FW_CUDA(launch_cell_select(h, d_logits, n_rows, step, sampler->mode, sampler->seed,
+                             sampler->stream_offset, d_out, static_cast<cudaStream_t>(stream)));
+  h.last_launches = 1;
   return FW_OK;
 }
 

@@ -22,6 +22,7 @@
 
 #include "internal.h"
 #include "tc_ptx.cuh"
+#include "select.cuh"
 
 namespace fw {
 namespace {
@@ -129,69 +130,6 @@ __device__ __forceinline__ float* cls_end(int* cls, int bt) {
   return reinterpret_cast<float*>(cls + ((bt + 3) & ~3));
 }
 
-__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
-
-// Warp-wide (value, index) maximum; ties go to the lower index (numpy argmax).
-__device__ __forceinline__ void warp_argmax(float& v, int& i) {
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-    float ov = __shfl_xor_sync(0xffffffffu, v, off);
-    int oi = __shfl_xor_sync(0xffffffffu, i, off);
-    if (ov > v || (ov == v && oi < i)) {
-      v = ov;
-      i = oi;
-    }
-  }
-}
-
-// Selection for one stream by one warp over A logits in smem.
-__device__ int select_class(const float* lg, int A, int mode, uint32_t prefix) {
-  const int lane = threadIdx.x & 31;
-  if (mode == FW_SAMPLE_INVCDF) {
-    float m = -INFINITY;
-    for (int a = lane; a < A; a += 32) m = fmaxf(m, lg[a]);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
-    // contiguous chunk per lane, sequential inside, scan across lanes
-    const int chunk = (A + 31) / 32;
-    const int a0 = min(A, lane * chunk), a1 = min(A, a0 + chunk);
-    float part = 0.f;
-    for (int a = a0; a < a1; ++a) part += expf(lg[a] - m);
-    float incl = part;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      float o = __shfl_up_sync(0xffffffffu, incl, off);
-      if (lane >= off) incl += o;
-    }
-    const float total = __shfl_sync(0xffffffffu, incl, 31);
-    const float thr = noise_uniform(prefix, kUniformClass) * total;
-    float run = incl - part;
-    int found = A;
-    for (int a = a0; a < a1; ++a) {
-      run += expf(lg[a] - m);
-      if (run > thr) {
-        found = a;
-        break;
-      }
-    }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, off));
-    return found < A ? found : A - 1;
-  }
-  float best = -INFINITY;
-  int bi = A;
-  for (int a = lane; a < A; a += 32) {
-    float v = lg[a];
-    if (mode == FW_SAMPLE_GUMBEL) v += -logf(-logf(noise_uniform(prefix, (uint32_t)a)));
-    if (v > best) {
-      best = v;
-      bi = a;
-    }
-  }
-  warp_argmax(best, bi);
-  return bi;
-}
-
 template <int BT, int NT>
 __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
   extern __shared__ float smem[];
@@ -227,7 +165,7 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
     // x_0 = E[c_t]; s = 0
     for (int e = tid; e < BT * R; e += NT) {
       const int b = e / R, r = e % R;
-      xx[b * 2 * R + r] = __ldg(p.w.embed + (size_t)cls[b] * R + r);
+      xx[b * 2 * R + r] = __ldg(p.w.embed + (size_t)clamp_class(cls[b], A) * R + r);
     }
     for (int e = tid; e < BT * S; e += NT) s[e] = 0.f;
     if (pre_pop) {
@@ -441,7 +379,7 @@ __global__ void __launch_bounds__(256) cell_cluster_kernel(SimtParams p) {
   __syncthreads();
   for (int i = 0; i < run.n_steps; ++i) {
     const int64_t t = run.t0 + i;
-    for (int r = tid; r < R; r += NT) xx[r] = __ldg(p.w.embed + (size_t)cls[0] * R + r);
+    for (int r = tid; r < R; r += NT) xx[r] = __ldg(p.w.embed + (size_t)clamp_class(cls[0], A) * R + r);
     for (int k = tid; k < Sc; k += NT) s_s[k] = 0.f;
     for (int e = tid; e < L * R; e += NT) xd_all[e] = *slot_ptr(e / R, t, e % R);
     cl_sync();  // every CTA has its pops before rank 0 pushes this step's inputs
@@ -932,7 +870,7 @@ __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p
     float* x0 = xx + ((i * L) & 1) * BT * 2 * R;
     for (int e = tid; e < BT * R; e += kStNT) {
       const int b = e / R, r = e % R;
-      x0[b * 2 * R + r] = __ldg(p.w.embed + (size_t)cls[b] * R + r);
+      x0[b * 2 * R + r] = __ldg(p.w.embed + (size_t)clamp_class(cls[b], A) * R + r);
     }
     for (int e = tid; e < BT * S; e += kStNT) s[e] = 0.f;
     if (i > 0)

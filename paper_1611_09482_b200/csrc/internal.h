@@ -39,6 +39,12 @@ __host__ __device__ __forceinline__ float noise_uniform(uint32_t prefix, uint32_
   return (static_cast<float>(h >> 8) + 0.5f) * (1.0f / 16777216.0f);
 }
 
+// Class id -> embedding row, kept inside [0, A): ids outside it (a caller bug the host
+// entry points and the Python shim reject) must not read past the embedding table.
+__host__ __device__ __forceinline__ int clamp_class(int c, int A) {
+  return (unsigned)c < (unsigned)A ? c : (c < 0 ? 0 : A - 1);
+}
+
 // ---- cell problem description ------------------------------------------------
 struct CellDims {
   int L, R, D, S, H, A;
@@ -94,6 +100,9 @@ void tc_set_trace(Handle& h, long long* trace);
 int64_t tc_debug_buffer(Handle& h, int which, const void** src);
 int cell_prefill(Handle& h, const int32_t* d_inputs, int T, float* d_logits, cudaStream_t st);
 void prefill_destroy(Handle& h);
+cudaError_t launch_cell_select(const Handle& h, const float* d_logits, int64_t n_rows, int64_t t0,
+                               int mode, uint32_t seed, int64_t stream_offset, int32_t* d_out,
+                               cudaStream_t st);
 
 struct PlainDev {
   int n_layers, w, act;

@@ -18,6 +18,8 @@ independent streams in lockstep (``fast_step`` then takes and returns arrays).
 
 from __future__ import annotations
 
+import weakref
+
 import ctypes as C
 from dataclasses import dataclass
 from typing import Sequence
@@ -273,12 +275,16 @@ _SCRATCH: dict = {}
 
 
 def _scratch_state(model: Model, batch: int, device) -> GenerationState:
+    """A device handle for compute_step's stateless evaluation, cached for the last model.
+    The cache holds a weak reference to the model and only hits for that very object: an
+    id() alone can be reused by a new model after the old one is collected."""
     key = (id(model), batch, device)
-    st = _SCRATCH.get(key)
-    if st is None or st.config != model.config:
-        st = GenerationState(model, batch, device)
-        _SCRATCH.clear()
-        _SCRATCH[key] = st
+    hit = _SCRATCH.get(key)
+    if hit is not None and hit[0]() is model:
+        return hit[1]
+    st = GenerationState(model, batch, device)
+    _SCRATCH.clear()
+    _SCRATCH[key] = (weakref.ref(model), st)
     return st
 
 

@@ -130,12 +130,24 @@ class CellGenerator:
             t = t.to(torch.int32)
         return t.contiguous()
 
+    def _check_classes(self, t) -> None:
+        """Input class ids must lie in [0, classes): the kernels index the embedding table
+        with them (out-of-range ids are clamped on the device, never read out of bounds, but
+        they are a caller error -- ValueError, as the reference's shape/arity checks)."""
+        if t.numel() == 0:
+            return
+        lo, hi = (int(v) for v in t.aminmax())
+        if lo < 0 or hi >= self.config.classes:
+            raise ValueError(f"input class ids must lie in [0, {self.config.classes}), "
+                             f"got [{lo}, {hi}]")
+
     def step(self, classes, sampler: Sampler = Sampler(), want_logits: bool = False,
              stream=None):
         """One cached step of every stream: returns (classes_out [B], logits [B, A] | None)."""
         import torch
 
         x = self._i32(classes).reshape(self.batch)
+        self._check_classes(x)
         out = torch.empty(self.batch, dtype=torch.int32, device=self._dev)
         lg = (torch.empty((self.batch, self.config.classes), dtype=torch.float32, device=self._dev)
               if want_logits else None)
@@ -147,16 +159,21 @@ class CellGenerator:
         return out, lg
 
     def generate(self, inputs, n_steps: int, sampler: Sampler = Sampler(),
-                 n_logit_steps: int = 0, out=None, logits=None, stream=None):
+                 n_logit_steps: int = 0, out=None, logits=None, stream=None,
+                 check_inputs: bool = True):
         """Device-side step loop; inputs (n_inputs, B) int32 on the GPU.
 
         Returns (classes (n_steps, B) int32, logits (n_logit_steps, B, A) | None).
+        ``check_inputs=False`` skips the class-range check (a device reduction and a host
+        sync) for inputs the caller has already validated.
         """
         import torch
 
         x = self._i32(inputs)
         if x.dim() != 2 or x.shape[1] != self.batch:
             raise ValueError("inputs must have shape (n_inputs, batch)")
+        if check_inputs:
+            self._check_classes(x)
         if out is None:
             out = torch.empty((n_steps, self.batch), dtype=torch.int32, device=self._dev)
         if n_logit_steps and logits is None:
@@ -179,6 +196,7 @@ class CellGenerator:
         x = self._i32(inputs)
         if x.dim() != 2 or x.shape[1] != self.batch:
             raise ValueError("inputs must have shape (T, batch)")
+        self._check_classes(x)
         T = int(x.shape[0])
         if want_logits and logits is None:
             logits = torch.empty((T, self.batch, self.config.classes), dtype=torch.float32,
@@ -188,12 +206,34 @@ class CellGenerator:
             C.c_void_p(logits.data_ptr() if want_logits else 0), _lib.stream_ptr(stream)))
         return logits if want_logits else None
 
+    def select(self, logits, step: int, sampler: Sampler = Sampler(), out=None, stream=None):
+        """The selection rule alone (fw_cell_select) over logits (n, B, A) or (B, A) fp32 on
+        the GPU: row (i, b) is stream b at step ``step + i``. Returns int32 classes of the
+        leading shape."""
+        import torch
+
+        lg = torch.as_tensor(logits, device=self._dev)
+        if lg.dtype != torch.float32 or lg.shape[-1] != self.config.classes or \
+                lg.shape[-2] != self.batch:
+            raise ValueError("logits must be float32 of shape (..., batch, classes)")
+        lg = lg.contiguous()
+        lead = lg.shape[:-1]
+        if out is None:
+            out = torch.empty(lead, dtype=torch.int32, device=self._dev)
+        s = sampler.c()
+        _lib.check(self._lib.fw_cell_select(
+            self._h, C.c_void_p(lg.data_ptr()), int(lg.numel() // self.config.classes),
+            int(step), C.byref(s), C.c_void_p(out.data_ptr()), _lib.stream_ptr(stream)))
+        return out
+
     def generate_host(self, inputs: np.ndarray, n_steps: int, sampler: Sampler = Sampler(),
                       out: np.ndarray | None = None, stream=None) -> np.ndarray:
         """Host in, host out: the end-to-end C-ABI entry (fw_cell_generate_host)."""
         x = np.ascontiguousarray(inputs, dtype=np.int32)
         if x.ndim != 2 or x.shape[1] != self.batch:
             raise ValueError("inputs must have shape (n_inputs, batch)")
+        if x.size and (x.min() < 0 or x.max() >= self.config.classes):
+            raise ValueError(f"input class ids must lie in [0, {self.config.classes})")
         if out is None:
             out = np.empty((n_steps, self.batch), dtype=np.int32)
         s = sampler.c()

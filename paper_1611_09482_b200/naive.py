@@ -66,7 +66,7 @@ class NaiveCellGenerator:
         n = p.shape[0]
         for _ in range(steps):
             lg = self.logits(hist[:n])
-            hist[n] = torch.argmax(lg, dim=1).to(torch.int32)
+            self._gen.select(lg, n - 1, out=hist[n])  # argmax, on the device (fw_cell_select)
             n += 1
         return hist[p.shape[0]:]
 

@@ -19,9 +19,13 @@ def histories(inputs: np.ndarray, choices: np.ndarray) -> np.ndarray:
 
 
 def check_streams(oracle: oc.CellOracle, inputs, choices, logits, streams, mode, seed,
-                  logit_tol, tie_tol, stream_offset=0, t0=0, report=None):
+                  logit_tol, tie_tol, stream_offset=0, t0=0, report=None, gids=None):
     """Compare GPU logits/choices of ``streams`` against the oracle run on the
     GPU's own input history (teacher-forced on it), SURVEY section 7.
+
+    ``inputs``/``choices``/``logits`` are indexed [step, column]; ``gids`` maps a column to
+    the global stream id that keys its noise (default: column + stream_offset), so callers
+    can pass a column subset of a large batch.
 
     Returns the number of near-tie choice mismatches (logged, allowed)."""
     hist = histories(np.asarray(inputs), np.asarray(choices))
@@ -34,7 +38,7 @@ def check_streams(oracle: oc.CellOracle, inputs, choices, logits, streams, mode,
             dev = np.max(np.abs(logits[:, s].astype(np.float64) - ref[:n_l]))
             worst = max(worst, dev)
             assert dev <= logit_tol, f"stream {s}: logits max-abs {dev:.3g} > {logit_tol}"
-        gsid = np.array([s + stream_offset])
+        gsid = np.array([gids[s] if gids is not None else s + stream_offset])
         for i in range(choices.shape[0]):
             want = oc.select(mode, ref[i:i + 1], seed, gsid, t0 + i)[0]
             got = int(choices[i, s])

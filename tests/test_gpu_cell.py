@@ -166,7 +166,8 @@ def test_tcgen05_matches_simt_all_streams_many_steps(cuda):
 def test_cfg5_deep_teacher_forced_walk(cuda):
     spec = configs.cfg5()
     m = build_cell_model(spec.cell)
-    n = 160  # first steps of the 48k-step run; cfg5's full 2,000-step check runs in bench.py --check
+    n = 160  # first steps of the 48k-step run; BASELINE's 2,000-step check (run to 2,100 steps,
+    # past the 2,048 ring wrap) is tests/test_gpu_long.py::test_cfg5_baseline_check_2100_steps
     walk = teacher_walk(n, spec.batch)
     gen = CellGenerator(m, spec.batch)
     out, lg = run(gen, walk, n, Sampler(0), n)
@@ -342,13 +343,18 @@ def test_staged_simt_kernel_matches_oracle_and_ldg_kernel(cuda, monkeypatch, bt)
         primer = cls[:3]
         for mode in (configs.SAMPLE_GUMBEL, configs.SAMPLE_INVCDF):
             s = Sampler(mode, 11)
+            tie = 2e-4 if mode == configs.SAMPLE_GUMBEL else 1e-5
             monkeypatch.setenv("FW_SIMT_STAGED", "1")
             got, _ = run(CellGenerator(m, B, kernel="simt"), primer, 40, s, 0)
             monkeypatch.setenv("FW_SIMT_STAGED", "0")
             monkeypatch.delenv("FW_SIMT_BT")
             want, _ = run(CellGenerator(m, B, kernel="simt"), primer, 40, s, 0)
             monkeypatch.setenv("FW_SIMT_BT", bt)
-            assert (got != want).mean() < 0.02, mode  # near-ties may flip a class, not the run
+            # both free runs: every choice is the oracle's on the kernel's own history, up
+            # to near-ties below the tolerance (a flipped near-tie forks the run, so the two
+            # kernels' sequences are each checked, not compared with each other)
+            for seq in (got, want):
+                check_streams(o, primer, seq, None, [0, B // 2, B - 1], mode, 11, 1e-4, tie)
 
 
 @pytest.mark.parametrize("sampler", [configs.SAMPLE_GUMBEL, configs.SAMPLE_ARGMAX])
@@ -363,6 +369,8 @@ def test_tcgen05_pair_tail_scores_folded_into_head2(cuda, sampler):
     s = Sampler(sampler, 21)
     folded, _ = run(CellGenerator(m, B, kernel="tcgen05"), primer, n, s, 0)
     plain, lg = run(CellGenerator(m, B, kernel="tcgen05"), primer, n, s, n)
-    assert (folded != plain).mean() < 0.01
-    check_streams(oc.CellOracle(m, exact=False), primer, plain, lg, [0, 200], sampler, 21,
+    o = oc.CellOracle(m, exact=False)
+    check_streams(o, primer, plain, lg, [0, 200], sampler, 21, *TOL["bf16"])
+    # the folded run (no logits): every choice margin-checked on its own history
+    check_streams(o, primer, folded, None, [0, 1, 127, 128, 200, 255], sampler, 21,
                   *TOL["bf16"])

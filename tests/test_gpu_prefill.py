@@ -211,3 +211,65 @@ def test_prefill_then_staged_kernel_continues(cuda, models):
     o = oc.CellOracle(models["simt"])
     for b in (0, 20):
         assert np.max(np.abs(ref[:, b] - o.forward_full(x[:, b]))) <= 1e-4
+
+
+@pytest.mark.parametrize("cfg", [CellConfig(1, 4, 4, 3, 5, classes=7, bias="fan_in", init_seed=3),
+                                 CellConfig(1, 5, 10, 6, 12, classes=11, dilation_base=3,
+                                            bias="fan_in", init_seed=9),
+                                 CellConfig(2, 2, 20, 20, 40, classes=300, bias="fan_in",
+                                            init_seed=1)])
+def test_prefill_odd_shapes(cuda, cfg):
+    """Channel counts that are not multiples of 8 (or 4) and classes != 256: the prefill
+    kernels move one channel per thread and the GEMM predicates its edges, so the result
+    matches stepping and the oracle exactly as for aligned shapes."""
+    m = build_cell_model(cfg)
+    B, T = 5, 70
+    x = np.random.default_rng(2).integers(0, cfg.classes, (T, B)).astype(np.int32)
+    ref_gen, ref = stepped(m, "simt", B, x)
+    gen = CellGenerator(m, B, kernel="simt")
+    lg = gen.prefill(torch.as_tensor(x, device="cuda"), want_logits=True).cpu().numpy()
+    assert np.max(np.abs(lg - ref)) <= 1e-4
+    assert np.max(np.abs(queue_values(gen) - queue_values(ref_gen))) <= 1e-4
+    o = oc.CellOracle(m)
+    for b in (0, B - 1):
+        assert np.max(np.abs(lg[:, b] - o.forward_full(x[:, b]))) <= 1e-4
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_select_matches_oracle_rules(cuda, models, mode):
+    """fw_cell_select (the selection stage alone) against oracle/cell.py's rules on random
+    logits: identical classes except near-ties (margin below 1e-5)."""
+    gen = CellGenerator(models["simt"], 3, kernel="simt")
+    lg = np.random.default_rng(mode).normal(0, 3, (20, 3, 256)).astype(np.float32)
+    got = gen.select(torch.as_tensor(lg, device="cuda"), 40, Sampler(mode, 17, 5)).cpu().numpy()
+    for i in range(20):
+        want = oc.select(mode, lg[i].astype(np.float64), 17, np.arange(3) + 5, 40 + i)
+        for b in range(3):
+            if want[b] != got[i, b]:
+                m = oc.selection_margin(mode, lg[i, b:b + 1].astype(np.float64), 17,
+                                        np.array([b + 5]), 40 + i, want[b:b + 1], got[i, b:b + 1])
+                assert m[0] <= 1e-5, (i, b, got[i, b], want[b])
+
+
+def test_out_of_range_classes_are_rejected(cuda, models):
+    gen = CellGenerator(models["simt"], 3, kernel="simt")
+    bad = torch.tensor([[1, 256, 3]], dtype=torch.int32, device="cuda")
+    with pytest.raises(ValueError):
+        gen.generate(bad, 2)
+    with pytest.raises(ValueError):
+        gen.step(torch.tensor([0, -1, 2], dtype=torch.int32, device="cuda"))
+    with pytest.raises(ValueError):
+        gen.prefill(bad)
+    with pytest.raises(ValueError):
+        gen.generate_host(np.array([[0, 1, 999]], dtype=np.int32), 2)
+    assert gen.step_index == 0
+    # the C ABI's host entry point checks the host buffer itself
+    import ctypes as C
+    from paper_1611_09482_b200 import _lib
+
+    h_in = np.array([[0, 1, 300]], dtype=np.int32)
+    h_out = np.empty((2, 3), dtype=np.int32)
+    s = Sampler(0).c()
+    rc = gen._lib.fw_cell_generate_host(gen._h, C.c_void_p(h_in.ctypes.data), 1, 2,
+                                        C.c_void_p(h_out.ctypes.data), C.byref(s), None)
+    assert rc == _lib.FW_ERR_INVALID
