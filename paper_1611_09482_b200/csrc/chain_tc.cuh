@@ -1042,7 +1042,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         // step i's input class: written by the pair's selection of step i-1
         if (i > 0) wait_counter(a.cls_ready + (tile >> 1), (uint32_t)i);
         trace_g(a, tr, 16);
-        const int c = clamp_class(a.cls[tile * kChainRows + row], a.sel.A);
+        const int c = clamp_class(a.cls[tile * kChainRows + row], 256);  // tc_supported: A = 256
         if (tr) {
           asm volatile("" ::"r"(c) : "memory");
           trace_g(a, true, 19);

@@ -9,6 +9,7 @@
 // all taps are read, which is ConvQueue.peek/pop/push of fast.py:57-88).
 // One CTA per stream; the step loop runs on the device.
 #include "internal.h"
+#include "libm_tanh.cuh"
 
 namespace fw {
 namespace {
@@ -40,7 +41,7 @@ __device__ void eval_layer(const PlainDev& p, int l, const double* prev, double*
       for (int c = 0; c < cin; ++c) acc = __dadd_rn(acc, __dmul_rn(row[c], v[c]));
     }
     acc = __dadd_rn(acc, bias[o]);
-    if (p.act == 1) acc = tanh(acc);
+    if (p.act == 1) acc = libm_tanh(acc);
     hout[o] = acc;
   }
 }
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(NT) plain_naive_kernel(PlainDev p, NaivePlan p
         }
       }
       acc = __dadd_rn(acc, bias[o]);
-      if (p.act == 1) acc = tanh(acc);
+      if (p.act == 1) acc = libm_tanh(acc);
       dst[(size_t)node * cout + o] = acc;
     }
     __syncthreads();

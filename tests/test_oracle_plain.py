@@ -95,3 +95,19 @@ def test_model_validation_mirrors_reference():
     assert receptive_field(ModelConfig(2, 3, filter_width=3, dilation_base=4)) == 1 + 2 * 2 * 21
     with pytest.raises(ValueError, match="finite"):
         LayerWeights(np.full((2, 1, 1), np.nan), np.zeros(1))
+
+
+def test_libm_tanh_restatement():
+    """oracle/libm_tanh.py (the algorithm csrc/libm_tanh.cuh ports to the device) equals the
+    host libm's tanh -- the one the reference's numba kernel calls -- bit for bit, on every
+    branch: tiny, |x| < 0.5 ln2 / 2 (k = 0), the k = -1 reduction, |x| >= 1, |x| >= 22."""
+    import math
+
+    from oracle.libm_tanh import tanh
+
+    rng = np.random.default_rng(7)
+    xs = 10.0 ** rng.uniform(-20, 1.6, 20_000) * rng.choice([-1.0, 1.0], 20_000)
+    xs = np.concatenate([xs, [0.0, -0.0, 5e-324, 22.0, -22.0, 21.999999, 1.0, -1.0,
+                              0.17328679513998632, 0.5198603854199589]])
+    bad = [x for x in xs if tanh(float(x)) != math.tanh(float(x))]
+    assert not bad, bad[:5]
