@@ -74,6 +74,7 @@ void free_cell(Handle& h) {
   h.d_qoff = nullptr;
   if (h.tc) tc_destroy(h);
   prefill_destroy(h);
+  lat_destroy(h);
   if (h.d_pad) cudaFree(h.d_pad);
   if (h.d_pad_lg) cudaFree(h.d_pad_lg);
   h.d_pad = nullptr;
@@ -314,6 +315,20 @@ int fw_cell_create(const fw_cell_desc* desc, int32_t batch, int32_t device, int3
   e = cudaMemset(h.d_queue, 0, (size_t)h.queue_bytes);
   if (e != cudaSuccess) return fail(cuda_fail(e, "queue zero-fill"));
 
+  // host copy (reference layouts, bf16-rounded where applicable) for lazily built images
+  {
+    HostCell& c = h.host;
+    c.dil_w = maybe_round(desc->dil_w, (size_t)L * 2 * 2 * D * R, bf);
+    c.dil_b = maybe_round(desc->dil_b, (size_t)L * 2 * D, bf);
+    c.res_w = maybe_round(desc->res_w, (size_t)L * R * D, bf);
+    c.res_b = maybe_round(desc->res_b, (size_t)L * R, bf);
+    c.skip_w = maybe_round(desc->skip_w, (size_t)L * S * D, bf);
+    c.skip_b = maybe_round(desc->skip_b, (size_t)L * S, bf);
+    c.h1_w = maybe_round(desc->head1_w, (size_t)H * S, bf);
+    c.h1_b = maybe_round(desc->head1_b, H, bf);
+    c.h2_w = maybe_round(desc->head2_w, (size_t)A * H, bf);
+    c.h2_b = maybe_round(desc->head2_b, A, bf);
+  }
   // SIMT weights (also used by the tcgen05 path for nothing but kept small)
   {
     std::vector<float> embed = maybe_round(desc->embed, (size_t)A * R, bf);

@@ -246,287 +246,20 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
   }
 }
 
-// ---- K1c: one stream per thread-block cluster (small batches) ------------------------------
-// At batch 1 a single CTA spends each layer waiting on L2 for weights it reads once per step
-// (one SM, latency-bound). Here the C CTAs of a cluster split every GEMV's outputs: each
-// streams 1/C of the weights, the z, x_{l+1}, ReLU(s), h and logits vectors are all-gathered
-// through distributed shared memory (st.shared::cluster) and one cluster barrier per
-// exchange orders them. Every CTA keeps the full x_l and selects the class redundantly
-// (deterministic), rank 0 writes the outputs and pushes the ring.
-__device__ __forceinline__ uint32_t cl_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cl_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-// v -> the same shared-memory float in CTA q of the cluster
-__device__ __forceinline__ void st_cl(float* p, uint32_t q, float v) {
-  uint32_t a;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;"
-               : "=r"(a)
-               : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(q));
-  asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
-}
-
-// out[o] = epi(o, sum_c W[c * ldw + o] * in[c]) for o < N <= NT (W already at the column
-// slice): K split over NT / N thread groups, partials reduced in a fixed order
-template <int NT, typename Epi>
-__device__ __forceinline__ void gemv_slice(const float* __restrict__ W, int ldw, int K, int N,
-                                           const float* in, float* red, Epi epi) {
-  const int tid = threadIdx.x;
-  const int G = NT / N;
-  const int o = tid % N, g = tid / N;
-  const int kc = (K + G - 1) / G, k0 = g * kc, k1 = min(K, k0 + kc);
-  if (g < G) {
-    float acc = 0.f;
-    int c = k0;
-    for (; c + 16 <= k1; c += 16) {
-      float w[16];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) w[j] = __ldg(W + (size_t)(c + j) * ldw + o);
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc = fmaf(w[j], in[c + j], acc);
-    }
-    for (; c < k1; ++c) acc = fmaf(__ldg(W + (size_t)c * ldw + o), in[c], acc);
-    red[g * N + o] = acc;
-  }
-  __syncthreads();
-  for (int e = tid; e < N; e += NT) {
-    float v = 0.f;
-    for (int gg = 0; gg < G; ++gg) v += red[gg * N + e];
-    epi(e, v);
-  }
-}
-
-// A GEMV whose weights are loaded into registers before its input exists (e.g. ahead of
-// the cluster barrier that publishes it): output o reads column col(o) of a matrix with
-// leading dimension ld(o), K split over NT / N thread groups (each group's share <= 32).
-struct ColMap {
-  const float* base0;  // outputs [0, n0): base0 + o, leading dimension ld0
-  int n0, ld0;
-  const float* base1;  // outputs [n0, N): base1 + (o - n0), leading dimension ld1
-  int ld1;
-};
-template <int NT>
-struct Prefetch {
-  float w[32];
-  int o, g, k0, k1, N, G;
-  __device__ __forceinline__ bool load(const ColMap& m, int K, int n) {
-    N = n;
-    G = NT / N;
-    o = threadIdx.x % N;
-    g = threadIdx.x / N;
-    const int kc = (K + G - 1) / G;
-    k0 = g * kc;
-    k1 = min(K, k0 + kc);
-    if (kc > 32) return false;
-    const float* col = o < m.n0 ? m.base0 + o : m.base1 + (o - m.n0);
-    const int ld = o < m.n0 ? m.ld0 : m.ld1;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) w[j] = (g < G && k0 + j < k1) ? __ldg(col + (size_t)(k0 + j) * ld) : 0.f;
-    return true;
-  }
-  template <typename Epi>
-  __device__ __forceinline__ void finish(const float* in, float* red, Epi epi) {
-    if (g < G) {
-      float acc = 0.f;
-#pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (k0 + j < k1) acc = fmaf(w[j], in[k0 + j], acc);
-      red[g * N + o] = acc;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < N; e += NT) {
-      float v = 0.f;
-      for (int gg = 0; gg < G; ++gg) v += red[gg * N + e];
-      epi(e, v);
-    }
-  }
-};
-
-template <int C>
-__global__ void __launch_bounds__(256) cell_cluster_kernel(SimtParams p) {
-  constexpr int NT = 256;
-  extern __shared__ float smem[];
-  const CellDims d = p.d;
-  const int R = d.R, D = d.D, S = d.S, H = d.H, A = d.A, L = d.L;
-  const int Dc = D / C, Rc = R / C, Sc = S / C, Hc = H / C, Ac = A / C;
-  const uint32_t rank = cl_rank();
-  const int stream = blockIdx.x / C;
-  float* xx = smem;              // [2R] x_l[t] | x_l[t-d] (full, every CTA)
-  float* xd_all = xx + 2 * R;    // [L][R] the step's pops
-  float* a_s = xd_all + L * R;   // [2 Dc] this CTA's tanh | sigmoid pre-activations
-  float* zf = a_s + 2 * Dc;      // [D] z, all-gathered
-  float* s_s = zf + D;           // [Sc] this CTA's skip-sum columns
-  float* sf = s_s + Sc;          // [S] ReLU(s), all-gathered
-  float* hf = sf + S;            // [H] h, all-gathered
-  float* lg = hf + H;            // [A] logits, all-gathered
-  float* red = lg + A;           // [NT]
-  int* cls = reinterpret_cast<int*>(red + NT);
-  const int tid = threadIdx.x;
-  const CellRun& run = p.run;
-  const int B = p.B;
-  const int Rp = (R + 3) & ~3;
-  const size_t slot_elems = (size_t)((B + 127) / 128) * 128 * Rp;
-  auto slot_ptr = [&](int l, int64_t t, int r) {
-    return p.queue + p.qoff[l] + (size_t)(t % p.dil[l]) * slot_elems +
-           ((size_t)((stream >> 7) * (Rp / 4) + (r >> 2)) * 128 + (stream & 127)) * 4 + (r & 3);
-  };
-  if (tid == 0) cls[0] = run.inputs[stream];
-  __syncthreads();
-  for (int i = 0; i < run.n_steps; ++i) {
-    const int64_t t = run.t0 + i;
-    for (int r = tid; r < R; r += NT) xx[r] = __ldg(p.w.embed + (size_t)clamp_class(cls[0], A) * R + r);
-    for (int k = tid; k < Sc; k += NT) s_s[k] = 0.f;
-    for (int e = tid; e < L * R; e += NT) xd_all[e] = *slot_ptr(e / R, t, e % R);
-    cl_sync();  // every CTA has its pops before rank 0 pushes this step's inputs
-    // the dilated GEMV's weights of layer 0 (later layers': prefetched a layer ahead)
-    Prefetch<NT> pd;
-    auto dil_map = [&](int l) {
-      const float* W = p.w.dilT + (size_t)l * 2 * R * 2 * D + (int)rank * Dc;
-      return ColMap{W, Dc, 2 * D, W + D, 2 * D};
-    };
-    bool pd_ok = pd.load(dil_map(0), 2 * R, 2 * Dc);
-    for (int l = 0; l < L; ++l) {
-      for (int r = tid; r < R; r += NT) {
-        xx[R + r] = xd_all[l * R + r];
-        if (rank == 0) *slot_ptr(l, t, r) = xx[r];  // push x_l[t] (its pop is in xd_all)
-      }
-      __syncthreads();
-      const float* db = p.w.dil_b + (size_t)l * 2 * D;
-      const int j0 = (int)rank * Dc;
-      // a = [tanh | sigmoid] pre-activations of this CTA's z columns, one GEMV
-      auto dil_epi = [&](int o, float v) {
-        a_s[o] = v + db[o < Dc ? j0 + o : D + j0 + (o - Dc)];
-      };
-      if (pd_ok) {
-        pd.finish(xx, red, dil_epi);
-      } else {
-        const float* W = p.w.dilT + (size_t)l * 2 * R * 2 * D;
-        gemv_slice<NT>(W + j0, 2 * D, 2 * R, Dc, xx, red, [&](int o, float v) { a_s[o] = v + db[j0 + o]; });
-        __syncthreads();
-        gemv_slice<NT>(W + D + j0, 2 * D, 2 * R, Dc, xx, red,
-                       [&](int o, float v) { a_s[Dc + o] = v + db[D + j0 + o]; });
-      }
-      __syncthreads();
-      // skip | residual columns of this CTA, weights in flight across the z exchange
-      const bool top = l + 1 >= L;
-      const int k0 = (int)rank * Sc, r0 = (int)rank * Rc;
-      const int nsr = Sc + (top ? 0 : Rc);
-      Prefetch<NT> psr;
-      const bool psr_ok = psr.load(ColMap{p.w.skipT + (size_t)l * D * S + k0, Sc, S,
-                                          p.w.resT + (size_t)l * D * R + r0, R},
-                                   D, nsr);
-      for (int j = tid; j < Dc; j += NT) {
-        const float z = tanhf(a_s[j]) * sigmoidf_(a_s[Dc + j]);
-        for (int q = 0; q < C; ++q) st_cl(zf + j0 + j, (uint32_t)q, z);
-      }
-      cl_sync();
-      const float* sb = p.w.skip_b + (size_t)l * S;
-      const float* rb = p.w.res_b + (size_t)l * R;
-      auto sr_epi = [&](int o, float v) {
-        if (o < Sc) {
-          s_s[o] += v + sb[k0 + o];
-        } else {
-          const int c = o - Sc;
-          const float xn = xx[r0 + c] + v + rb[r0 + c];
-          for (int q = 0; q < C; ++q) st_cl(xx + r0 + c, (uint32_t)q, xn);
-        }
-      };
-      if (psr_ok) {
-        psr.finish(zf, red, sr_epi);
-      } else {
-        gemv_slice<NT>(p.w.skipT + (size_t)l * D * S + k0, S, D, Sc, zf, red,
-                       [&](int o, float v) { s_s[o] += v + sb[k0 + o]; });
-        if (!top) {
-          __syncthreads();
-          gemv_slice<NT>(p.w.resT + (size_t)l * D * R + r0, R, D, Rc, zf, red,
-                         [&](int o, float v) { sr_epi(Sc + o, v); });
-        }
-      }
-      if (!top) {
-        pd_ok = pd.load(dil_map(l + 1), 2 * R, 2 * Dc);  // next layer's, across the exchange
-        cl_sync();  // x_{l+1} in every CTA
-      } else {
-        __syncthreads();
-      }
-    }
-    // head: logits = W2 ReLU(W1 ReLU(s) + b1) + b2
-    for (int k = tid; k < Sc; k += NT) {
-      const float v = fmaxf(s_s[k], 0.f);
-      for (int q = 0; q < C; ++q) st_cl(sf + rank * Sc + k, (uint32_t)q, v);
-    }
-    cl_sync();
-    gemv_slice<NT>(p.w.h1T + rank * Hc, H, S, Hc, sf, red, [&](int o, float v) {
-      const float h = fmaxf(v + p.w.h1_b[rank * Hc + o], 0.f);
-      for (int q = 0; q < C; ++q) st_cl(hf + rank * Hc + o, (uint32_t)q, h);
-    });
-    cl_sync();
-    gemv_slice<NT>(p.w.h2T + rank * Ac, A, H, Ac, hf, red, [&](int o, float v) {
-      const float x = v + p.w.h2_b[rank * Ac + o];
-      for (int q = 0; q < C; ++q) st_cl(lg + rank * Ac + o, (uint32_t)q, x);
-    });
-    cl_sync();
-    if (rank == 0 && run.logits != nullptr && i < run.n_logit_steps) {
-      float* dst = run.logits + ((size_t)i * B + stream) * A;
-      for (int e = tid; e < A; e += NT) dst[e] = lg[e];
-    }
-    if (tid < 32) {
-      const uint32_t gs = (uint32_t)(run.stream_offset + stream);
-      const uint32_t prefix = noise_prefix(run.seed, gs, (uint32_t)t);
-      const int c = select_class(lg, A, run.mode, prefix);
-      if (tid == 0) {
-        if (rank == 0) run.out[(size_t)i * B + stream] = c;
-        cls[0] = (i + 1 < run.n_inputs) ? run.inputs[(size_t)(i + 1) * B + stream] : c;
-      }
-    }
-    // every CTA selected the same class; its lg / hf / sf are rewritten only after the
-    // next step's cluster barriers
-    __syncthreads();
-  }
-  cl_sync();  // no DSMEM writes into a CTA that has exited
-}
-
-// Cluster size for a stream count (0: the per-CTA kernel): every slice must divide evenly
+// Cluster size for a stream count (0: no cluster kernel): the small-batch kernel
+// (cell_lat.cu) splits every GEMV's outputs over the C CTAs of a cluster, so every slice
+// must divide evenly
 int cluster_for(const CellDims& d, int B) {
   if (const char* e = getenv("FW_SIMT_CLUSTER")) return atoi(e);
-  // measured (tools/depth_sweep.py, tools/bench_prefill.py): 8-CTA clusters win at one
-  // stream (cfg2 L=14: 417 -> 75 us/step); at 64 streams (cfg3) two-CTA clusters lose to the
-  // per-CTA kernel (521 vs 433 us/step), so only up to 16 streams go to clusters
+  // one stream per cluster pays off while the streams fit the SMs as clusters (up to 16
+  // streams at 8 CTAs each); past that the weight-staged kernel shares each weight load
+  // between several streams
   const int want = B <= 16 ? 8 : 0;
   for (int c = want; c >= 2; c /= 2)
-    if (d.D % c == 0 && d.R % c == 0 && d.S % c == 0 && d.H % c == 0 && d.A % c == 0 &&
-        d.A / c <= 256 && d.S / c <= 256 && d.H / c <= 256 && d.D / c <= 256 && d.R / c <= 256)
-      return c;
+    if (lat_supported(d, c)) return c;
   return 0;
 }
 
-template <int C>
-cudaError_t launch_cluster(const SimtParams& p, cudaStream_t st) {
-  const CellDims& d = p.d;
-  const size_t sm = sizeof(float) * (size_t)(2 * d.R + d.L * d.R + 2 * d.D / C + d.D + d.S / C +
-                                             d.S + d.H + d.A + 256) + 16;
-  cudaError_t e = cudaFuncSetAttribute(cell_cluster_kernel<C>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p.B * C);
-  cfg.blockDim = dim3(256);
-  cfg.dynamicSmemBytes = sm;
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = C;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  void* args[] = {const_cast<SimtParams*>(&p)};
-  return cudaLaunchKernelExC(&cfg, (const void*)cell_cluster_kernel<C>, args);
-}
 
 // ---- K1s: weight-staged fp32 kernel (mid batches, fp32 configs 3 and 5) -----------------
 // The per-CTA kernel above reads every weight with __ldg and spends most of a layer waiting on
@@ -996,7 +729,7 @@ cudaError_t launch_bt(const SimtParams& p, cudaStream_t st) {
 
 }  // namespace
 
-cudaError_t launch_cell_simt(const Handle& h, const CellRun& run, cudaStream_t st,
+cudaError_t launch_cell_simt(Handle& h, const CellRun& run, cudaStream_t st,
                              int64_t* launches) {
   SimtParams p;
   p.d = h.dims;
@@ -1010,14 +743,10 @@ cudaError_t launch_cell_simt(const Handle& h, const CellRun& run, cudaStream_t s
   // Streams per CTA: enough CTAs to cover the SMs, up to 8 streams sharing
   // each weight load.
   const int B = h.batch;
-  // small batches: one cluster of 2..8 CTAs per stream (FW_SIMT_CLUSTER overrides)
-  if (h.dims.L * h.dims.R <= 16384) {
-    switch (cluster_for(h.dims, B)) {
-      case 8: return launch_cluster<8>(p, st);
-      case 4: return launch_cluster<4>(p, st);
-      case 2: return launch_cluster<2>(p, st);
-      default: break;
-    }
+  // small batches: one cluster of 2..16 CTAs per stream (FW_SIMT_CLUSTER overrides)
+  if (const int c = cluster_for(h.dims, B)) {
+    const cudaError_t e = launch_cell_lat(h, run, c, st);
+    if (e != cudaErrorNotSupported) return e;
   }
   // mid/large batches: the weight-staged kernel (FW_SIMT_STAGED=0 selects the __ldg kernel)
   const char* se = getenv("FW_SIMT_STAGED");

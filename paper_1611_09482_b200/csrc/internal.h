@@ -82,16 +82,27 @@ struct SimtWeights {
   float* h2_b;   // [A]
 };
 
+// Host copy of the cell's weights in the reference layouts (fw_cell_desc), rounded to bf16
+// for bf16 configs: the source of the per-kernel images built lazily after create.
+struct HostCell {
+  std::vector<float> dil_w, dil_b, res_w, res_b, skip_w, skip_b, h1_w, h1_b, h2_w, h2_b;
+};
+
 // tcgen05 path device state (see cell_tc.cu).
 struct TcState;
+// small-batch cluster kernel's packed weights (see cell_lat.cu).
+struct LatPlan;
 // full-sequence prefill state (see prefill.cu).
 struct PrefillState;
 
 struct Handle;
 
 // Launchers (return cudaError_t of the launch); defined in the kernel files.
-cudaError_t launch_cell_simt(const Handle& h, const CellRun& run, cudaStream_t st,
+cudaError_t launch_cell_simt(Handle& h, const CellRun& run, cudaStream_t st,
                              int64_t* launches);
+cudaError_t launch_cell_lat(Handle& h, const CellRun& run, int C, cudaStream_t st);
+bool lat_supported(const CellDims& d, int C);
+void lat_destroy(Handle& h);
 cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64_t* launches);
 bool tc_supported(const CellDims& d, int batch, std::string* why);
 int tc_create(Handle& h, const fw_cell_desc* desc);
@@ -164,6 +175,8 @@ struct Handle {
   SimtWeights w{};
   TcState* tc = nullptr;
   PrefillState* prefill = nullptr;
+  LatPlan* lat = nullptr;
+  HostCell host;
 
   // plain
   PlainDev p{};

@@ -178,7 +178,7 @@ __global__ void select_rows(const float* __restrict__ logits, int64_t n, int B, 
 constexpr int kBM = 128, kBN = 128, kBK = 16, kGemmNT = 256;
 
 template <typename T>
-__global__ void __launch_bounds__(kGemmNT) gemm_rows(const T* __restrict__ A, const T* __restrict__ W,
+__global__ void __launch_bounds__(kGemmNT, 2) gemm_rows(const T* __restrict__ A, const T* __restrict__ W,
                                                      float* __restrict__ C, int64_t n, int K, int N,
                                                      int accumulate) {
   __shared__ __align__(16) float As[2][kBK][kBM];

@@ -240,7 +240,7 @@ def test_invalid_arguments(cuda, cfg1_model):
     assert cell_fast_generate(cfg1_model, [1], 0).shape == (1, 0)
 
 
-@pytest.mark.parametrize("cluster", ["0", "2", "4", "8"])
+@pytest.mark.parametrize("cluster", ["0", "2", "4", "8", "16"])
 def test_small_batch_cluster_kernel_matches_oracle(cuda, cfg1_model, monkeypatch, cluster):
     """The cluster-per-stream SIMT kernel (FW_SIMT_CLUSTER) and the per-CTA kernel give the
     oracle's teacher-forced logits on the same inputs, for 1 and 3 streams."""
@@ -374,3 +374,21 @@ def test_tcgen05_pair_tail_scores_folded_into_head2(cuda, sampler):
     # the folded run (no logits): every choice margin-checked on its own history
     check_streams(o, primer, folded, None, [0, 1, 127, 128, 200, 255], sampler, 21,
                   *TOL["bf16"])
+
+
+@pytest.mark.parametrize("cluster", ["2", "8", "16"])
+def test_small_batch_kernel_streamed_weights(cuda, monkeypatch, cluster):
+    """The small-batch cluster kernel with weights streamed through its two-slot ring (cfg2's
+    128-channel layers do not fit shared memory), non-zero biases (folded into the next
+    layer's taps), teacher-forced logits against the oracle past the ring wraps of d <= 32."""
+    monkeypatch.setenv("FW_SIMT_CLUSTER", cluster)
+    cfg = CellConfig(1, 6, 128, 128, 256, bias="fan_in", init_seed=12)
+    m = build_cell_model(cfg)
+    B, n = 2, 80
+    cls = np.random.default_rng(8).integers(0, 256, (n, B))
+    out, lg = run(CellGenerator(m, B, kernel="simt"), cls, n, Sampler(0), n)
+    o = oc.CellOracle(m)
+    for b in range(B):
+        ref = o.forward_full(cls[:, b])
+        assert np.max(np.abs(lg[:, b] - ref)) <= 1e-4, (cluster, b)
+        assert np.array_equal(out[:, b], np.argmax(lg[:, b], axis=1))

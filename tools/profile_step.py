@@ -15,6 +15,9 @@ gen = CellGenerator(build_cell_model(spec.cell), batch,
                     kernel="tcgen05" if spec.cell.weight_dtype == "bf16" else "simt")
 primer = torch.full((1, batch), spec.primer_class, dtype=torch.int32, device="cuda")
 gen.generate(primer, steps, Sampler(spec.sampler, configs.NOISE_SEED))  # warm-up launch
+torch.cuda.synchronize()
+torch.cuda.profiler.start()  # range for ncu --replay-mode (app-)range --profile-from-start off
 gen.generate(primer, steps, Sampler(spec.sampler, configs.NOISE_SEED))  # profiled launch
 torch.cuda.synchronize()
+torch.cuda.profiler.stop()
 print(f"profiled: {steps} steps of {spec.name} in one launch")
