@@ -203,8 +203,10 @@ int fw_last_launch_count(const fw_handle* h, int64_t* out);
 int fw_destroy(fw_handle* h);
 const char* fw_last_error(void);
 /* Diagnostics: record per-layer clock64() phase timestamps of CTA 0 of the
- * tcgen05 chain kernel into d_trace [n_layers][16] (NULL disables). Not part
- * of the reference's interface; used by tools/trace_chain.py. */
+ * tcgen05 chain kernel into d_trace [n_layers][16] (NULL disables); on a SIMT handle the
+ * small-batch cluster kernel instead writes %globaltimer stamps of its phases in step 1
+ * of a launch, d_trace [n_layers + 4][8]. Not part of the reference's interface; used by
+ * tools/trace_chain.py and tools/trace_lat.py. */
 int fw_debug_trace(fw_handle* h, int64_t* d_trace);
 /* Diagnostics: copy the first `bytes` of an internal device buffer to d_dst on `stream`.
  * which = 0: the HBM ring queues (layout in DESIGN.md); tcgen05 handles only: 1 z stash,

@@ -696,7 +696,10 @@ int fw_reset(fw_handle* fh, void* stream) {
 int fw_debug_trace(fw_handle* fh, int64_t* d_trace) {
   int rc = check_handle(fh, false);
   if (rc) return rc;
-  if (fh->h.kernel != FW_KERNEL_TCGEN05) return invalid("phase trace needs the tcgen05 path");
+  if (fh->h.kernel != FW_KERNEL_TCGEN05) {
+    fh->h.lat_trace = reinterpret_cast<long long*>(d_trace);  // small-batch kernel
+    return FW_OK;
+  }
   tc_set_trace(fh->h, reinterpret_cast<long long*>(d_trace));
   return FW_OK;
 }

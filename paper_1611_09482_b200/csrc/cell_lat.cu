@@ -41,8 +41,8 @@ namespace fw {
 
 namespace {
 
-constexpr int kLatNT = 256;  // 8 warps
-constexpr int kLatPad = 64;  // zero floats after every input vector (padded GEMV rows)
+constexpr int kLatNT = 512;   // 16 warps: the phases are latency-bound, more lanes per GEMV
+constexpr int kLatPad = 128;  // zero floats after every input vector (padded GEMV rows)
 
 // Per-C packed weights and their layout (host-computed, uploaded once per handle and C).
 struct LatLayout {
@@ -52,10 +52,12 @@ struct LatLayout {
   int Kprs, lpo_rs;      // res | skip rows over z (K = D)
   int Kph1, lpo_h1;      // head1 over ReLU(s) (K = S)
   int Kph2, lpo_h2;      // head2 over h (K = H)
+  int lg_d, lg_rs, lg_h1, lg_h2;  // log2 of the lanes per output
   // float offsets inside a phase block
   int64_t o_dil, o_bd, o_rs, o_br, o_bs, phase_floats;
   int64_t post_floats;   // block L: skip rows + bias
-  int64_t h1_floats, h2_floats;
+  int64_t h1_floats, h2_floats;  // one head block: rows (h1r / h2r of the slice) + biases
+  int h1p, h2p, h1r, h2r;          // head slices split into parts of at most h1r / h2r rows
   int64_t step_floats;      // all blocks of a step (per rank)
   int64_t max_block;
   int resident;
@@ -80,6 +82,7 @@ struct LatParams {
   const float* w;  // this launch's packed weights [C][step_floats]
   LatLayout lay;
   CellRun run;
+  long long* trace;  // diagnostics: [phase][8] globaltimer stamps of CTA 0 in step 1, or null
 };
 
 __device__ __forceinline__ uint32_t lat_rank() {
@@ -111,26 +114,113 @@ __device__ __forceinline__ void lat_bcast(const float* p, float v) {
 // out[o] = sum_k W[o * Kp + k] * in[k] for o < n (LPO lanes per output, k = sub + LPO i,
 // two accumulators, fixed-order shuffle reduction); epi(o, v) on the output's lane sub 0.
 // Also returns v to every lane of the output group (for the gate's pair exchange).
+// out[o] = sum_k W[o * Kp + k] * in[k] for o < n: LPO lanes per output, lane `sub` takes the
+// 16-byte chunks k = 4 (sub + LPO i) .. +3 (LDS.128 of weights and inputs; rows padded so
+// a warp's chunks fall in distinct banks, inputs padded with zeros past K), two
+// accumulators, fixed-order shuffle reduction; epi(o, v, sub, lpo) on every lane.
 template <typename Epi>
-__device__ __forceinline__ void lat_gemv(const float* W, int Kp, int K, int n, int lpo,
+__device__ __forceinline__ void lat_gemv(const float* W, int Kp, int K, int n, int lg_lpo,
                                          const float* in, Epi epi) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int opw = 32 / lpo, sub = lane & (lpo - 1);
+  const int lpo = 1 << lg_lpo, opw = 32 >> lg_lpo, sub = lane & (lpo - 1);
+  const float4* in4 = reinterpret_cast<const float4*>(in);
   for (int o0 = warp * opw; o0 < n; o0 += (kLatNT / 32) * opw) {
-    const int o = o0 + lane / lpo;
+    const int o = o0 + (lane >> lg_lpo);
     float a0 = 0.f, a1 = 0.f;
     if (o < n) {
-      const float* w = W + (int64_t)o * Kp;
-      int k = sub;
-      for (; k + lpo < K; k += 2 * lpo) {
-        a0 = fmaf(w[k], in[k], a0);
-        a1 = fmaf(w[k + lpo], in[k + lpo], a1);
+      const float4* w4 = reinterpret_cast<const float4*>(W + (int64_t)o * Kp);
+      int c = sub;  // 16-byte chunk index
+      const int nc = (K + 3) >> 2;
+      for (; c + lpo < nc; c += 2 * lpo) {
+        const float4 w0 = w4[c], x0 = in4[c], w1 = w4[c + lpo], x1 = in4[c + lpo];
+        a0 = fmaf(w0.x, x0.x, a0);
+        a1 = fmaf(w1.x, x1.x, a1);
+        a0 = fmaf(w0.y, x0.y, a0);
+        a1 = fmaf(w1.y, x1.y, a1);
+        a0 = fmaf(w0.z, x0.z, a0);
+        a1 = fmaf(w1.z, x1.z, a1);
+        a0 = fmaf(w0.w, x0.w, a0);
+        a1 = fmaf(w1.w, x1.w, a1);
       }
-      if (k < K) a0 = fmaf(w[k], in[k], a0);
+      if (c < nc) {
+        const float4 w0 = w4[c], x0 = in4[c];
+        a0 = fmaf(w0.x, x0.x, a0);
+        a0 = fmaf(w0.y, x0.y, a0);
+        a0 = fmaf(w0.z, x0.z, a0);
+        a0 = fmaf(w0.w, x0.w, a0);
+      }
     }
     float v = a0 + a1;
     for (int off = lpo >> 1; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
     epi(o, v, sub, lpo);
+  }
+}
+
+// fp32 gate, MUFU-based: tanh(a) = 1 - 2 / (e^{2a} + 1), sigmoid(g) = 1 / (1 + e^{-g});
+// absolute error ~1e-7 (the SIMT configs' logits tolerance is 1e-4)
+__device__ __forceinline__ float lat_gate(float a, float g) {
+  const float th = 1.f - 2.f * __frcp_rn(__expf(2.f * a) + 1.f);
+  return th * __frcp_rn(1.f + __expf(-g));
+}
+
+// Asynchronous remote store: v -> shared::cluster address `addr`, completing `bytes` of the
+// transaction count of the receiver's mbarrier `mbar` (also a shared::cluster address).
+__device__ __forceinline__ void lat_st_async(uint32_t addr, float v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(addr),
+               "r"(__float_as_uint(v)), "r"(mbar)
+               : "memory");
+}
+// Wait for a phase of a local mbarrier completed by other CTAs' st.async transactions: the
+// data is shared memory of this CTA, so a CTA-scope acquire suffices (a cluster-scope one
+// would also invalidate L1 -- CCTL.IVALL -- on every exchange).
+__device__ __forceinline__ void lat_wait(uint64_t* bar, uint32_t parity) { ptx::mbar_wait(bar, parity); }
+__device__ __forceinline__ long long lat_now() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// One exchange: this CTA's staged slices -> the same floats of every CTA of the cluster,
+// signalling each receiver's mbarrier `bar`. Up to three segments (src, dst, n) flattened
+// into one index space so every thread issues at most a few remote stores (a st.async is
+// not free to issue: ~ the DSMEM round trip).
+struct LatSeg {
+  const float* src;
+  float* dst;
+  int n;
+};
+__device__ __forceinline__ void lat_st_async4(uint32_t addr, float4 v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(addr),
+               "r"(__float_as_uint(v.x)), "r"(__float_as_uint(v.y)), "r"(__float_as_uint(v.z)),
+               "r"(__float_as_uint(v.w)), "r"(mbar)
+               : "memory");
+}
+// items (16-byte chunks when the segment allows it, else single floats) of one segment
+__device__ __forceinline__ int lat_items(const LatSeg& s) {
+  const bool v4 = (s.n & 3) == 0 && ((reinterpret_cast<uintptr_t>(s.dst) | reinterpret_cast<uintptr_t>(s.src)) & 15) == 0;
+  return v4 ? s.n >> 2 : s.n;
+}
+template <int C>
+__device__ __forceinline__ void lat_send1(const LatSeg& s, int f, uint32_t bar_local) {
+  const int k = f / C;
+  const uint32_t q = (uint32_t)(f - k * C);
+  const uint32_t mbar = lat_mapa(reinterpret_cast<const float*>(__cvta_shared_to_generic(bar_local)), q);
+  if (lat_items(s) != s.n)
+    lat_st_async4(lat_mapa(s.dst + 4 * k, q), reinterpret_cast<const float4*>(s.src)[k], mbar);
+  else
+    lat_st_async(lat_mapa(s.dst + k, q), s.src[k], mbar);
+}
+template <int C>
+__device__ __forceinline__ void lat_send(LatSeg a, LatSeg b, LatSeg c, uint64_t* bar) {
+  const int na = lat_items(a) * C, nb = lat_items(b) * C, nall = na + nb + lat_items(c) * C;
+  const uint32_t bl = ptx::smem_u32(bar);
+  for (int e = threadIdx.x; e < nall; e += kLatNT) {
+    if (e < na)
+      lat_send1<C>(a, e, bl);
+    else if (e < na + nb)
+      lat_send1<C>(b, e - na, bl);
+    else
+      lat_send1<C>(c, e - na - nb, bl);
   }
 }
 
@@ -145,49 +235,70 @@ __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
   const int stream = blockIdx.x / C;
   const int tid = threadIdx.x;
   const int j0 = (int)rank * Dc, r0 = (int)rank * Rc, k0 = (int)rank * Sc;
-  // shared memory: weights | inbuf[2][2R + D + pad] | xall[L][R] | s[Sc] | sf[S + pad] |
-  // hf[H + pad] | lg[A] | cls
+  const int h0 = (int)rank * Hc, a0 = (int)rank * Ac;
+  // shared memory: weights | barriers (ring [2], exchange [2]) | inbuf[2][2R + D + pad] |
+  // staged slices (z, x, x_{t-d}, ReLU(s), h, logits) | s[Sc] | sf[S + pad] | hf[H + pad] |
+  // lg[A] | cls
   float* wsm = smem;
   const int64_t wfl = Y.resident ? Y.step_floats : 2 * Y.max_block;
-  const int in_len = 2 * R + D + kLatPad;
-  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + wfl);  // [2] ring slots (16-byte aligned)
-  float* inbuf = wsm + wfl + 4;
-  float* xall = inbuf + 2 * in_len;
-  float* s_s = xall + L * R;
+  const int in_len = (2 * R + D + kLatPad + 3) & ~3;
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + wfl);  // [2] weight ring slots
+  uint64_t* xbar = full + 2;                                  // [2] exchanges (alternating)
+  float* inbuf = wsm + wfl + 8;
+  // staged outputs of this CTA (<= Dc + 2 Rc or Sc + Rc, Hc, Ac), double-buffered by
+  // exchange parity: a thread still sending exchange e reads them while the fastest thread
+  // can already be writing exchange e + 1's (it cannot reach e + 2 before every thread of
+  // this CTA has sent e + 1)
+  float* stg2 = inbuf + 2 * in_len;
+  const int stg_len = (max(max(Dc + 2 * Rc, Sc + Rc), max(Hc, Ac)) + 3) & ~3;
+  float* s_s = stg2 + 2 * stg_len;
   float* sf = s_s + ((Sc + 3) & ~3);
-  float* hf = sf + S + kLatPad;
-  float* lg = hf + H + kLatPad;
+  float* hf = sf + ((S + kLatPad + 3) & ~3);
+  float* lg = hf + ((H + kLatPad + 3) & ~3);
   int* cls = reinterpret_cast<int*>(lg + A);
+  // this step's ring slot base (element offset) of every layer, + layer 0's of the next step
+  int64_t* rslot = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(cls + 4) + 7) & ~(uintptr_t)7);
   const float* wg = p.w + (int64_t)rank * Y.step_floats;  // this rank's blocks in global
-  const int nblk = L + 3;
+  // blocks of a step: L phases, the top skip, h1p parts of head1, h2p parts of head2
+  const int nblk = L + 1 + Y.h1p + Y.h2p;
   auto block_off = [&](int b) -> int64_t {  // float offset of block b inside a step
-    return b <= L ? (int64_t)b * Y.phase_floats
-                  : (int64_t)L * Y.phase_floats + Y.post_floats + (b == L + 2 ? Y.h1_floats : 0);
+    if (b <= L) return (int64_t)b * Y.phase_floats;
+    const int64_t hb = (int64_t)L * Y.phase_floats + Y.post_floats;
+    const int p = b - L - 1;
+    return p < Y.h1p ? hb + p * Y.h1_floats : hb + Y.h1p * Y.h1_floats + (p - Y.h1p) * Y.h2_floats;
   };
   auto block_len = [&](int b) -> int64_t {
-    return b < L ? Y.phase_floats : (b == L ? Y.post_floats : (b == L + 1 ? Y.h1_floats : Y.h2_floats));
+    return b < L ? Y.phase_floats : (b == L ? Y.post_floats : (b - L - 1 < Y.h1p ? Y.h1_floats : Y.h2_floats));
   };
   const CellRun& run = p.run;
   const int B = p.B;
   const int Rp = (R + 3) & ~3;
   const size_t slot_elems = (size_t)((B + 127) / 128) * 128 * Rp;
-  auto ring_ptr = [&](int l, int64_t t, int r) {
-    return p.queue + p.qoff[l] + (size_t)(t % p.dil[l]) * slot_elems +
-           ((size_t)((stream >> 7) * (Rp / 4) + (r >> 2)) * 128 + (stream & 127)) * 4 + (r & 3);
+  const int64_t soff = (int64_t)(stream >> 7) * (Rp / 4) * 512 + (stream & 127) * 4;
+  auto ring_at = [&](int64_t base, int r) {  // channel r of this stream in the slot at `base`
+    return p.queue + base + soff + (int64_t)(r >> 2) * 512 + (r & 3);
+  };
+  auto slot_base = [&](int l, int64_t t) { return p.qoff[l] + (t % p.dil[l]) * (int64_t)slot_elems; };
+  // control duties (weight-ring copies, exchange arming, trace stamps) sit on the last
+  // thread, which owns no ring channel and (for up to kLatNT - 1 items) sends nothing
+  const int ctl = kLatNT - 1;
+  const bool tracer = p.trace != nullptr && blockIdx.x == 0 && tid == ctl;
+  auto stamp = [&](int i, int ph, int k) {
+    if (tracer && i == 1) p.trace[ph * 8 + k] = lat_now();
   };
 
   // zero the padded tails of the input vectors (the padded weight columns are zero, so the
-  // pads must be finite), load resident weights, init the ring barriers
+  // pads must be finite); barriers; resident weights
   for (int e = tid; e < 2 * in_len; e += kLatNT) inbuf[e] = 0.f;
   for (int e = tid; e < S + kLatPad; e += kLatNT) sf[e] = 0.f;
   for (int e = tid; e < H + kLatPad; e += kLatNT) hf[e] = 0.f;
-  if (tid == 0) {
-    ptx::mbar_init(&full[0], 1);
-    ptx::mbar_init(&full[1], 1);
+  if (tid == ctl) {
+    for (int k = 0; k < 4; ++k) ptx::mbar_init(&full[k], 1);
     ptx::fence_mbar_init();
   }
-  __syncthreads();
-  int64_t g = 0;  // blocks consumed (ring mode)
+  // every CTA's exchange barriers exist before any remote store targets them
+  lat_cluster_sync();
+  int64_t g = 0;  // weight blocks consumed (ring mode)
   auto issue = [&](int64_t gi) {  // ring: block gi of the launch into slot gi & 1
     const int b = (int)(gi % nblk);
     const uint32_t bytes = (uint32_t)(block_len(b) * 4);
@@ -195,125 +306,185 @@ __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
     ptx::mbar_arrive_expect_tx(&full[gi & 1], bytes);
     ptx::bulk_g2s(wsm + (gi & 1) * Y.max_block, wg + block_off(b), bytes, &full[gi & 1]);
   };
-  if (Y.resident) {
-    if (tid == 0) {
+  if (tid == ctl) {
+    if (Y.resident) {
       const uint32_t bytes = (uint32_t)(Y.step_floats * 4);
       ptx::mbar_arrive_expect_tx(&full[0], bytes);
       ptx::bulk_g2s(wsm, wg, bytes, &full[0]);
+    } else {
+      issue(0);
     }
-  } else if (tid == 0) {
-    issue(0);
   }
-  // block b of the current step, waited for
+  // block b of the current step, waited for; the next block's copy goes into the slot the
+  // previous phase released (every phase ends with a CTA barrier before its sends)
   auto take = [&](int b) -> const float* {
     if (Y.resident) return wsm + block_off(b);
     ptx::mbar_wait(&full[g & 1], (uint32_t)((g >> 1) & 1));
     const float* w = wsm + (g & 1) * Y.max_block;
-    if (tid == 0 && g + 1 < (int64_t)run.n_steps * nblk) issue(g + 1);
+    if (tid == ctl && g + 1 < (int64_t)run.n_steps * nblk) issue(g + 1);
     ++g;
     return w;
   };
   if (Y.resident) ptx::mbar_wait(&full[0], 0);
-  // pops of the first step (each CTA keeps every layer's x_{t-d}; later steps' pops are
-  // loaded during the previous step's heads, after its last push)
-  for (int e = tid; e < L * R; e += kLatNT) xall[e] = __ldcg(ring_ptr(e / R, run.t0, e % R));
+  // exchange e of the launch completes on xbar[e & 1]; this CTA arms it with the bytes it
+  // will receive (transactions that arrive first drive the count negative until then)
+  int64_t ex = 0;
+  auto arm = [&](int64_t e, int floats) {
+    if (tid == ctl)  // relaxed: orders nothing this thread did before (it sent nothing)
+      asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(
+                       ptx::smem_u32(&xbar[e & 1])), "r"((uint32_t)(floats * 4))
+                   : "memory");
+  };
+  auto wait_ex = [&](int64_t e) { lat_wait(&xbar[e & 1], (uint32_t)((e >> 1) & 1)); };
+  // the first step's x_0[t-d] (later steps': exchanged with ReLU(s) of the step before)
+  for (int r = tid; r < R; r += kLatNT) inbuf[R + r] = __ldcg(ring_at(slot_base(0, run.t0), r));
   if (tid == 0) cls[0] = run.inputs[stream];
   __syncthreads();
 
   for (int i = 0; i < run.n_steps; ++i) {
     const int64_t t = run.t0 + i;
-    // phase 0 input: x_0 = E[c_t] (z part: any finite value, its weights are zero), x_0[t-d]
+    const bool more = i + 1 < run.n_steps;
+    // phase 0 input: x_0 = E[c_t] (z part: any finite value, its weights are zero); the
+    // step's ring slots (one modulo per layer per step)
     {
       const float* e = p.embed + (size_t)clamp_class(cls[0], A) * R;
-      for (int r = tid; r < R; r += kLatNT) {
-        inbuf[r] = __ldg(e + r);
-        inbuf[R + r] = xall[r];
-      }
+      for (int r = tid; r < R; r += kLatNT) inbuf[r] = __ldg(e + r);
       for (int k = tid; k < Sc; k += kLatNT) s_s[k] = 0.f;
+      for (int l = tid; l <= L; l += kLatNT) rslot[l] = l < L ? slot_base(l, t) : slot_base(0, t + 1);
     }
     __syncthreads();
     for (int l = 0; l < L; ++l) {
+      // ring pops and pushes of channel r0 + tid are this thread's alone (tid < Rc): it reads
+      // back only its own earlier stores (program order, no cross-CTA fence); the pop of
+      // the next layer's slot is issued first, its value is needed at the end of the phase
+      const bool pop = l + 1 < L;
+      float popv = 0.f;
+      if (pop && tid < Rc) popv = __ldcg(ring_at(rslot[l + 1], r0 + tid));
+      stamp(i, l, 0);
+      if (l > 0) wait_ex(ex - 1);  // x_{l-1}, z_{l-1}, x_l[t-d_l] from every CTA
+      stamp(i, l, 1);
       const float* wb = take(l);
       const float* in = inbuf + (l & 1) * in_len;
       float* nxt = inbuf + ((l + 1) & 1) * in_len;
+      float* stg = stg2 + (ex & 1) * stg_len;
+      // data of the next phase (or the top layer's z for the skip): armed before this CTA
+      // sends its own part of it
+      arm(ex, D + R + (pop ? R : 0));
       // dilated taps (+ folded residual) of this CTA's z columns; rows 2j / 2j+1 = the
       // tanh / sigmoid pre-activation of column j0 + j
       const float* bd = wb + Y.o_bd;
-      lat_gemv(wb + Y.o_dil, Y.Kpd, Y.Kd, 2 * Dc, Y.lpo_d, in, [&](int o, float v, int sub, int lpo) {
+      lat_gemv(wb + Y.o_dil, Y.Kpd, Y.Kd, 2 * Dc, Y.lg_d, in, [&](int o, float v, int sub, int lpo) {
         const float pv = __shfl_down_sync(0xffffffffu, v, lpo);  // the sigmoid row's sum
-        if (o < 2 * Dc && sub == 0 && (o & 1) == 0) {
-          const float z = tanhf(v + bd[o]) * sigmoidf_(pv + bd[o + 1]);
-          lat_bcast<C>(nxt + 2 * R + j0 + (o >> 1), z);
-        }
+        if (o < 2 * Dc && sub == 0 && (o & 1) == 0)
+          stg[o >> 1] = lat_gate(v + bd[o], pv + bd[o + 1]);
       });
-      // x_l slice (residual of the previous layer; x_0 itself at l = 0) -> ring l and every
-      // CTA; s slice += skip of the previous layer
+      stamp(i, l, 2);
+      // x_l slice (residual of the previous layer; x_0 itself at l = 0); s slice += skip of
+      // the previous layer
       const float* br = wb + Y.o_br;
       const float* bs = wb + Y.o_bs;
-      lat_gemv(wb + Y.o_rs, Y.Kprs, D, Rc + Sc, Y.lpo_rs, in + 2 * R, [&](int o, float v, int sub, int) {
+      lat_gemv(wb + Y.o_rs, Y.Kprs, D, Rc + Sc, Y.lg_rs, in + 2 * R, [&](int o, float v, int sub, int) {
         if (o < Rc + Sc && sub == 0) {
-          if (o < Rc) {
-            const float x = in[r0 + o] + v + br[o];
-            lat_bcast<C>(nxt + r0 + o, x);
-            *ring_ptr(l, t, r0 + o) = x;  // push x_l[t] (its pop was read before this step)
-          } else if (l > 0) {
+          if (o < Rc)
+            stg[Dc + o] = in[r0 + o] + v + br[o];
+          else if (l > 0)
             s_s[o - Rc] += v + bs[o - Rc];
-          }
         }
       });
-      // the next phase's x_{l+1}[t-d]
-      if (l + 1 < L)
-        for (int r = tid; r < R; r += kLatNT) nxt[R + r] = xall[(l + 1) * R + r];
-      lat_cluster_sync();
+      stamp(i, l, 3);
+      if (pop && tid < Rc) stg[Dc + Rc + tid] = popv;
+      stamp(i, l, 4);
+      __syncthreads();  // every warp is done with `in` and the staged slices are complete
+      stamp(i, l, 5);
+      lat_send<C>(LatSeg{stg, nxt + 2 * R + j0, Dc}, LatSeg{stg + Dc, nxt + r0, Rc},
+                  LatSeg{stg + Dc + Rc, nxt + R + r0, pop ? Rc : 0}, &xbar[ex & 1]);
+      stamp(i, l, 6);
+      if (tid < Rc) *ring_at(rslot[l], r0 + tid) = stg[Dc + tid];  // push x_l[t]
+      stamp(i, l, 7);
+      ++ex;
     }
-    // the top layer's skip: s += W_skip,L-1 z_{L-1} + b
+    // the top layer's skip: s += W_skip,L-1 z_{L-1} + b; ReLU(s) (+ the next step's
+    // x_0[t+1-d_0] slice, popped by the thread that pushed it) to every CTA
     {
+      float popv = 0.f;
+      if (more && tid < Rc) popv = __ldcg(ring_at(rslot[L], r0 + tid));
+      stamp(i, L, 0);
+      wait_ex(ex - 1);
+      stamp(i, L, 1);
       const float* wb = take(L);
       const float* in = inbuf + (L & 1) * in_len;
-      lat_gemv(wb, Y.Kprs, D, Sc, Y.lpo_rs, in + 2 * R, [&](int o, float v, int sub, int) {
-        if (o < Sc && sub == 0) {
-          const float s = s_s[o] + v + wb[(int64_t)Sc * Y.Kprs + o];
-          lat_bcast<C>(sf + k0 + o, fmaxf(s, 0.f));
-        }
+      float* stg = stg2 + (ex & 1) * stg_len;
+      arm(ex, S + (more ? R : 0));
+      lat_gemv(wb, Y.Kprs, D, Sc, Y.lg_rs, in + 2 * R, [&](int o, float v, int sub, int) {
+        if (o < Sc && sub == 0) stg[o] = fmaxf(s_s[o] + v + wb[(int64_t)Sc * Y.Kprs + o], 0.f);
       });
+      stamp(i, L, 2);
+      if (more && tid < Rc) stg[Sc + tid] = popv;
+      stamp(i, L, 4);
+      __syncthreads();
+      stamp(i, L, 5);
+      lat_send<C>(LatSeg{stg, sf + k0, Sc}, LatSeg{stg + Sc, inbuf + R + r0, more ? Rc : 0},
+                  LatSeg{stg, stg, 0}, &xbar[ex & 1]);
+      stamp(i, L, 6);
+      ++ex;
     }
-    // every push of this step is done (barrier L-1): the next step's pops
-    if (i + 1 < run.n_steps)
-      for (int e = tid; e < L * R; e += kLatNT) xall[e] = __ldcg(ring_ptr(e / R, t + 1, e % R));
-    lat_cluster_sync();
+    stamp(i, L + 1, 0);
+    wait_ex(ex - 1);
+    stamp(i, L + 1, 1);
     {
-      const float* wb = take(L + 1);
-      const int h0 = (int)rank * Hc;
-      lat_gemv(wb, Y.Kph1, S, Hc, Y.lpo_h1, sf, [&](int o, float v, int sub, int) {
-        if (o < Hc && sub == 0) lat_bcast<C>(hf + h0 + o, fmaxf(v + wb[(int64_t)Hc * Y.Kph1 + o], 0.f));
-      });
+      float* stg = stg2 + (ex & 1) * stg_len;
+      arm(ex, H);
+      for (int part = 0; part < Y.h1p; ++part) {  // rows [part * h1r, ...) of the slice
+        const float* wb = take(L + 1 + part);
+        const int o0 = part * Y.h1r, n = min(Y.h1r, Hc - o0);
+        lat_gemv(wb, Y.Kph1, S, n, Y.lg_h1, sf, [&](int o, float v, int sub, int) {
+          if (o < n && sub == 0) stg[o0 + o] = fmaxf(v + wb[(int64_t)Y.h1r * Y.Kph1 + o], 0.f);
+        });
+        if (part + 1 < Y.h1p) __syncthreads();  // the ring slot is reused two parts on
+      }
+      __syncthreads();
+      lat_send<C>(LatSeg{stg, hf + h0, Hc}, LatSeg{stg, stg, 0}, LatSeg{stg, stg, 0}, &xbar[ex & 1]);
+      ++ex;
     }
-    lat_cluster_sync();
+    stamp(i, L + 2, 0);
+    wait_ex(ex - 1);
+    stamp(i, L + 2, 1);
     {
-      const float* wb = take(L + 2);
-      const int a0 = (int)rank * Ac;
+      float* stg = stg2 + (ex & 1) * stg_len;
+      arm(ex, A);
       float* dst = (run.logits != nullptr && i < run.n_logit_steps)
                        ? run.logits + ((size_t)i * B + stream) * A + a0 : nullptr;
-      lat_gemv(wb, Y.Kph2, H, Ac, Y.lpo_h2, hf, [&](int o, float v, int sub, int) {
-        if (o < Ac && sub == 0) {
-          const float x = v + wb[(int64_t)Ac * Y.Kph2 + o];
-          lat_bcast<C>(lg + a0 + o, x);
-          if (dst) dst[o] = x;
-        }
-      });
+      for (int part = 0; part < Y.h2p; ++part) {
+        const float* wb = take(L + 1 + Y.h1p + part);
+        const int o0 = part * Y.h2r, n = min(Y.h2r, Ac - o0);
+        lat_gemv(wb, Y.Kph2, H, n, Y.lg_h2, hf, [&](int o, float v, int sub, int) {
+          if (o < n && sub == 0) {
+            const float x = v + wb[(int64_t)Y.h2r * Y.Kph2 + o];
+            stg[o0 + o] = x;
+            if (dst) dst[o0 + o] = x;
+          }
+        });
+        if (part + 1 < Y.h2p) __syncthreads();
+      }
+      __syncthreads();
+      lat_send<C>(LatSeg{stg, lg + a0, Ac}, LatSeg{stg, stg, 0}, LatSeg{stg, stg, 0}, &xbar[ex & 1]);
+      ++ex;
     }
-    lat_cluster_sync();
+    stamp(i, L + 3, 0);
+    wait_ex(ex - 1);
+    stamp(i, L + 3, 1);
     if (tid < 32) {
       const uint32_t prefix = noise_prefix(run.seed, (uint32_t)(run.stream_offset + stream), (uint32_t)t);
       const int c = select_class(lg, A, run.mode, prefix);
       if (tid == 0) {
         if (rank == 0) run.out[(size_t)i * B + stream] = c;
-        cls[0] = (i + 1 < run.n_inputs) ? run.inputs[(size_t)(i + 1) * B + stream] : c;
+        cls[0] = more && i + 1 < run.n_inputs ? run.inputs[(size_t)(i + 1) * B + stream] : c;
       }
     }
     __syncthreads();
+    stamp(i, L + 3, 2);
   }
-  lat_cluster_sync();  // no DSMEM writes into a CTA that has exited
+  lat_cluster_sync();  // no remote stores into a CTA that has exited
 }
 
 int pow2_floor(int v) {
@@ -327,13 +498,23 @@ int lpo_for(int n, int max_lpo) {
   int lpo = pow2_floor(std::max(1, kLatNT / std::max(n, 1)));
   return std::max(1, std::min(lpo, max_lpo));
 }
-// row stride: K rounded to a multiple of the lanes per output, then to lpo (mod 32) so the
-// 32 / lpo rows a warp reads start in distinct banks
+// row stride (floats): K rounded up to whole chunks of every lane of an output group
+// (4 lpo floats, at least 32), then offset so the 16-byte chunks a quarter-warp loads -- 8 / lpo
+// rows, lpo consecutive chunks each -- land in distinct bank groups
 int kpad(int K, int lpo) {
-  const int k32 = (K + 31) / 32 * 32;
-  return lpo >= 32 ? k32 : k32 + lpo;
+  const int q = std::max(32, 4 * lpo);
+  const int kr = (K + q - 1) / q * q;
+  return lpo < 8 ? kr + 4 * lpo : kr;
 }
 int64_t up4(int64_t v) { return (v + 3) & ~(int64_t)3; }  // 16-byte granules
+
+// shared memory beside the weights (floats): barriers, inbuf, staged slices, s, sf, hf,
+// lg, cls -- the kernel's carve-up
+int64_t lat_act_floats(const CellDims& d, const LatLayout& Y) {
+  const int64_t stg = up4(std::max(std::max(Y.Dc + 2 * Y.Rc, Y.Sc + Y.Rc), std::max(Y.Hc, Y.Ac)));
+  return 8 + 2 * up4(2 * d.R + d.D + kLatPad) + 2 * stg + up4(Y.Sc) + up4(d.S + kLatPad) + up4(d.H + kLatPad) +
+         d.A + 4 + 2 * (d.L + 1) + 2;
+}
 
 }  // namespace
 
@@ -375,6 +556,15 @@ static int lat_prepare(Handle& h, int C, std::string* err) {
   Y.Kph1 = kpad(S, Y.lpo_h1);
   Y.lpo_h2 = lpo_for(Y.Ac, 32);
   Y.Kph2 = kpad(H, Y.lpo_h2);
+  auto lg2 = [](int v) {
+    int r = 0;
+    while ((1 << r) < v) ++r;
+    return r;
+  };
+  Y.lg_d = lg2(Y.lpo_d);
+  Y.lg_rs = lg2(Y.lpo_rs);
+  Y.lg_h1 = lg2(Y.lpo_h1);
+  Y.lg_h2 = lg2(Y.lpo_h2);
   Y.o_dil = 0;
   Y.o_bd = up4((int64_t)2 * Y.Dc * Y.Kpd);
   Y.o_rs = Y.o_bd + up4(2 * Y.Dc);
@@ -382,13 +572,25 @@ static int lat_prepare(Handle& h, int C, std::string* err) {
   Y.o_bs = Y.o_br + up4(Y.Rc);
   Y.phase_floats = Y.o_bs + up4(Y.Sc);
   Y.post_floats = up4((int64_t)Y.Sc * Y.Kprs) + up4(Y.Sc);
-  Y.h1_floats = up4((int64_t)Y.Hc * Y.Kph1) + up4(Y.Hc);
-  Y.h2_floats = up4((int64_t)Y.Ac * Y.Kph2) + up4(Y.Ac);
-  Y.step_floats = (int64_t)L * Y.phase_floats + Y.post_floats + Y.h1_floats + Y.h2_floats;
+  // head slices in parts no larger than a phase block (the ring's slot size), so a config
+  // with wide heads and narrow layers (cfg3) still streams through two slots
+  const int64_t cap = std::max(Y.phase_floats, Y.post_floats);
+  auto parts = [&](int rows, int Kp, int* np, int* rpp, int64_t* fl) {
+    *np = 1;
+    *rpp = rows;
+    while (*rpp > 1 && up4((int64_t)*rpp * Kp) + up4(*rpp) > cap) {
+      ++*np;
+      *rpp = (rows + *np - 1) / *np;
+    }
+    *np = (rows + *rpp - 1) / *rpp;
+    *fl = up4((int64_t)*rpp * Kp) + up4(*rpp);
+  };
+  parts(Y.Hc, Y.Kph1, &Y.h1p, &Y.h1r, &Y.h1_floats);
+  parts(Y.Ac, Y.Kph2, &Y.h2p, &Y.h2r, &Y.h2_floats);
+  Y.step_floats = (int64_t)L * Y.phase_floats + Y.post_floats + Y.h1p * Y.h1_floats + Y.h2p * Y.h2_floats;
   Y.max_block = std::max(std::max(Y.phase_floats, Y.post_floats), std::max(Y.h1_floats, Y.h2_floats));
   // activations + barriers beside the weights; resident when a step's blocks fit
-  const int64_t act_floats = 2 * (2 * R + D + kLatPad) + (int64_t)L * R + up4(Y.Sc) + S + kLatPad +
-                             H + kLatPad + A + 4 + 8;
+  const int64_t act_floats = lat_act_floats(d, Y);
   const int64_t budget = 220 * 1024 / 4;
   Y.resident = (Y.step_floats + act_floats <= budget && Y.step_floats * 4 < (1u << 20)) ? 1 : 0;
   if (!Y.resident && 2 * Y.max_block + act_floats > budget) {
@@ -443,13 +645,17 @@ static int lat_prepare(Handle& h, int C, std::string* err) {
     }
     float* h1 = post + Y.post_floats;
     for (int o = 0; o < Y.Hc; ++o) {
-      for (int k = 0; k < S; ++k) h1[(int64_t)o * Y.Kph1 + k] = w.h1_w[(size_t)(q * Y.Hc + o) * S + k];
-      h1[(int64_t)Y.Hc * Y.Kph1 + o] = w.h1_b[q * Y.Hc + o];
+      float* part = h1 + (o / Y.h1r) * Y.h1_floats;
+      const int ro = o % Y.h1r;
+      for (int k = 0; k < S; ++k) part[(int64_t)ro * Y.Kph1 + k] = w.h1_w[(size_t)(q * Y.Hc + o) * S + k];
+      part[(int64_t)Y.h1r * Y.Kph1 + ro] = w.h1_b[q * Y.Hc + o];
     }
-    float* h2 = h1 + Y.h1_floats;
+    float* h2 = h1 + Y.h1p * Y.h1_floats;
     for (int o = 0; o < Y.Ac; ++o) {
-      for (int k = 0; k < H; ++k) h2[(int64_t)o * Y.Kph2 + k] = w.h2_w[(size_t)(q * Y.Ac + o) * H + k];
-      h2[(int64_t)Y.Ac * Y.Kph2 + o] = w.h2_b[q * Y.Ac + o];
+      float* part = h2 + (o / Y.h2r) * Y.h2_floats;
+      const int ro = o % Y.h2r;
+      for (int k = 0; k < H; ++k) part[(int64_t)ro * Y.Kph2 + k] = w.h2_w[(size_t)(q * Y.Ac + o) * H + k];
+      part[(int64_t)Y.h2r * Y.Kph2 + ro] = w.h2_b[q * Y.Ac + o];
     }
   }
   cudaError_t e = cudaMalloc(&Y.d_w, sizeof(float) * img.size());
@@ -465,9 +671,7 @@ static int lat_prepare(Handle& h, int C, std::string* err) {
 
 static size_t lat_smem_bytes(const CellDims& d, const LatLayout& Y) {
   const int64_t wfl = Y.resident ? Y.step_floats : 2 * Y.max_block;
-  const int64_t act = 2 * (2 * d.R + d.D + kLatPad) + (int64_t)d.L * d.R + ((Y.Sc + 3) & ~3) +
-                      d.S + kLatPad + d.H + kLatPad + d.A + 4 + 4;  // + 2 mbarriers, + cls
-  return sizeof(float) * (size_t)(wfl + act) + 16;
+  return sizeof(float) * (size_t)(wfl + lat_act_floats(d, Y)) + 16;
 }
 
 template <int C>
@@ -516,6 +720,7 @@ cudaError_t launch_cell_lat(Handle& h, const CellRun& run, int C, cudaStream_t s
   p.w = h.lat->lay.d_w;
   p.lay = h.lat->lay;
   p.run = run;
+  p.trace = h.lat_trace;
   const size_t smem = lat_smem_bytes(h.dims, p.lay);
   switch (C) {
     case 2: return lat_launch<2>(p, smem, st);

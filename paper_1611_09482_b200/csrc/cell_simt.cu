@@ -251,12 +251,11 @@ __global__ void __launch_bounds__(NT) cell_simt_kernel(SimtParams p) {
 // must divide evenly
 int cluster_for(const CellDims& d, int B) {
   if (const char* e = getenv("FW_SIMT_CLUSTER")) return atoi(e);
-  // one stream per cluster pays off while the streams fit the SMs as clusters (up to 16
-  // streams at 8 CTAs each); past that the weight-staged kernel shares each weight load
-  // between several streams
-  const int want = B <= 16 ? 8 : 0;
-  for (int c = want; c >= 2; c /= 2)
-    if (lat_supported(d, c)) return c;
+  // one stream per cluster while the clusters fit the SMs side by side (B * C <= 148: up to
+  // 9 streams at 16 CTAs ... 74 at 2); past that the weight-staged kernel shares each weight
+  // load between several streams
+  for (int c = 16; c >= 2; c /= 2)
+    if ((int64_t)B * c <= 148 && lat_supported(d, c)) return c;
   return 0;
 }
 

@@ -176,6 +176,7 @@ struct Handle {
   TcState* tc = nullptr;
   PrefillState* prefill = nullptr;
   LatPlan* lat = nullptr;
+  long long* lat_trace = nullptr;  // fw_debug_trace on a SIMT handle: small-batch kernel stamps
   HostCell host;
 
   // plain
