@@ -118,13 +118,16 @@ __device__ __forceinline__ void lat_bcast(const float* p, float v) {
 // 16-byte chunks k = 4 (sub + LPO i) .. +3 (LDS.128 of weights and inputs; rows padded so
 // a warp's chunks fall in distinct banks, inputs padded with zeros past K), two
 // accumulators, fixed-order shuffle reduction; epi(o, v, sub, lpo) on every lane.
+// The warps [w0, w0 + nw) of the CTA compute it (the layer phases run the dilated GEMV and
+// the residual/skip GEMV side by side on the two halves of the CTA).
 template <typename Epi>
 __device__ __forceinline__ void lat_gemv(const float* W, int Kp, int K, int n, int lg_lpo,
-                                         const float* in, Epi epi) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+                                         const float* in, Epi epi, int w0 = 0, int nw = kLatNT / 32) {
+  const int warp = (threadIdx.x >> 5) - w0, lane = threadIdx.x & 31;
+  if (warp < 0 || warp >= nw) return;
   const int lpo = 1 << lg_lpo, opw = 32 >> lg_lpo, sub = lane & (lpo - 1);
   const float4* in4 = reinterpret_cast<const float4*>(in);
-  for (int o0 = warp * opw; o0 < n; o0 += (kLatNT / 32) * opw) {
+  for (int o0 = warp * opw; o0 < n; o0 += nw * opw) {
     const int o = o0 + (lane >> lg_lpo);
     float a0 = 0.f, a1 = 0.f;
     if (o < n) {
@@ -373,11 +376,12 @@ __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
       // dilated taps (+ folded residual) of this CTA's z columns; rows 2j / 2j+1 = the
       // tanh / sigmoid pre-activation of column j0 + j
       const float* bd = wb + Y.o_bd;
+      constexpr int kHalf = kLatNT / 64;  // warps per GEMV of a layer phase
       lat_gemv(wb + Y.o_dil, Y.Kpd, Y.Kd, 2 * Dc, Y.lg_d, in, [&](int o, float v, int sub, int lpo) {
         const float pv = __shfl_down_sync(0xffffffffu, v, lpo);  // the sigmoid row's sum
         if (o < 2 * Dc && sub == 0 && (o & 1) == 0)
           stg[o >> 1] = lat_gate(v + bd[o], pv + bd[o + 1]);
-      });
+      }, 0, kHalf);
       stamp(i, l, 2);
       // x_l slice (residual of the previous layer; x_0 itself at l = 0); s slice += skip of
       // the previous layer
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
           else if (l > 0)
             s_s[o - Rc] += v + bs[o - Rc];
         }
-      });
+      }, kHalf, kHalf);
       stamp(i, l, 3);
       if (pop && tid < Rc) stg[Dc + Rc + tid] = popv;
       stamp(i, l, 4);
@@ -494,8 +498,8 @@ int pow2_floor(int v) {
 }
 // lanes per output so that the n outputs fill the CTA's 8 warps (at least 2 outputs per warp
 // when pairs must share a warp)
-int lpo_for(int n, int max_lpo) {
-  int lpo = pow2_floor(std::max(1, kLatNT / std::max(n, 1)));
+int lpo_for(int n, int max_lpo, int threads = kLatNT) {
+  int lpo = pow2_floor(std::max(1, threads / std::max(n, 1)));
   return std::max(1, std::min(lpo, max_lpo));
 }
 // row stride (floats): K rounded up to whole chunks of every lane of an output group
@@ -548,9 +552,9 @@ static int lat_prepare(Handle& h, int C, std::string* err) {
   Y.Hc = H / C;
   Y.Ac = A / C;
   Y.Kd = 2 * R + D;
-  Y.lpo_d = lpo_for(2 * Y.Dc, 16);  // a z column's two rows in one warp
+  Y.lpo_d = lpo_for(2 * Y.Dc, 16, kLatNT / 2);  // a z column's two rows in one warp
   Y.Kpd = kpad(Y.Kd, Y.lpo_d);
-  Y.lpo_rs = lpo_for(Y.Rc + Y.Sc, 32);
+  Y.lpo_rs = lpo_for(Y.Rc + Y.Sc, 32, kLatNT / 2);
   Y.Kprs = kpad(D, Y.lpo_rs);
   Y.lpo_h1 = lpo_for(Y.Hc, 32);
   Y.Kph1 = kpad(S, Y.lpo_h1);
