@@ -41,6 +41,7 @@ struct TcState {
   uint32_t* zflag = nullptr;  // [5][B/128] fused counters: z stash | s | h | selections | z reads
   int64_t* d_qoff = nullptr;  // [L] byte offset of each layer's ring
   int fused = 0, SK = 256, nchain = 0, nskip = 0;
+  int split = 0;              // chain tiles split over 2-CTA clusters (small batches)
   int heads = 0;              // head1 / head2 fused into the skip blocks (needs fused)
   uint8_t* wh1b = nullptr;    // [nsk][S/64][H/nsk rows][128 B] (fused head1)
   uint8_t* wh1 = nullptr;     // [H/128][S/64] chunks of [128][64]
@@ -164,6 +165,8 @@ struct ChainArgs {
   // + selection by its first skip block; sflag / hflag count the blocks done with simg / himg
   int heads, H;
   int pair_mode;         // tail blocks in 2-CTA clusters exchanging through DSMEM
+  int split;             // chain tiles over 2-CTA clusters, one dilated N-half per CTA
+  int zpub;              // z stash publications per tile pair per layer (2, or 4 when split)
   uint32_t* sflag;       // [B/128] (cumulative over the launch's steps)
   uint32_t* hflag;       // [B/128]
   const uint8_t* wh1b;   // [nsk][S/64][H/nsk rows][128 B]
@@ -721,6 +724,12 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
     // too; other shapes keep per-step launches with the skip / head GEMM kernels
     tc->heads = tc->fused && (H % nsk == 0) && (n1 == 128 || n1 == 256);
     tc->fused = tc->heads;
+    // split chain: each 64-stream tile over a 2-CTA cluster, one dilated N-half per CTA
+    // (needs the pair tail's cluster launch and room for twice the chain CTAs)
+    const char* se = getenv("FW_CHAIN_SPLIT");
+    tc->split = tc->heads && S == 512 && H == 512 && A == 256 && 2 * tc->nchain + tc->nskip <= sms &&
+                !(se && atoi(se) == 0) && !getenv("FW_NO_CLUSTER");
+    if (tc->split) tc->nchain *= 2;
     if (tc->heads) {
       std::vector<uint8_t> w1((size_t)nsk * (S / 64) * n1 * 128);
       for (int e = 0; e < nsk; ++e)
@@ -798,7 +807,9 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.has_res_bias = tc->has_res_bias;
   ca.trace = tc->trace;
   const int npairs_all = B / 128;
-  ca.nchain = B / kChainRows;
+  ca.nchain = tc->nchain;
+  ca.split = tc->split;
+  ca.zpub = tc->split ? 4 : 2;
   ca.zflag = tc->fused ? tc->zflag : nullptr;
   // z stash: a 16-layer ring per pair in the fused kernel (the unfused skip GEMM reads all L)
   ca.zring = tc->fused ? std::min(L, 16) : L;

@@ -51,6 +51,13 @@
 // x_full -> next layer's x_{t-d} N-half 1.
 
 constexpr int kChainRows = 64;
+// split chain: the z half crosses to the peer by bulk copies (async proxy end to end) when
+// set, by st.async stores otherwise
+#ifndef FW_SPLIT_BULK
+#define FW_SPLIT_BULK 1
+#endif
+constexpr bool kSplitBulk = FW_SPLIT_BULK != 0;
+
 constexpr int kChainThreads = 512;  // 16 warps; 128 registers per thread (4 warps per SMSP)
 constexpr int kQueueWarp0 = 10;
 constexpr uint32_t kP1 = 16u << 16;  // lane offset of plane P1
@@ -79,9 +86,12 @@ constexpr uint32_t kTailStage = 2 * (kTile + 32768);  // 2 K-chunks of A | 2 of 
 constexpr int kTailStages = 2;
 // chain role: after its barriers, two 16 KB staging buffers for popped ring slots
 constexpr uint32_t kOffXq = kOffBars + 1024;
+// chain role: after the pop staging, two 16 KB staging images of the layer's z tile
+// ([16 K-pieces][64 rows][16 B]) that the publisher bulk-stores into the z stash
+constexpr uint32_t kOffZs = kOffXq + 2 * kSlotBytes;
 constexpr size_t kSmemMax3(size_t a, size_t b, size_t c) { return a > b ? (a > c ? a : c) : (b > c ? b : c); }
 constexpr size_t kChainSmem =
-    1024 + kSmemMax3(kOffXq + 2 * kSlotBytes, kSkipBars + 8448, kPairBias + 1024);
+    1024 + kSmemMax3(kOffZs + 2 * kSlotBytes, kSkipBars + 8448, kPairBias + 1024);
 
 // z stash row base of (tile, ring slot): [tile pair][zring][16 pieces][128 rows][16 B]. The
 // fused kernel keeps a ring of zring (< L) layers per pair -- small enough to stay in L2,
@@ -183,7 +193,7 @@ __device__ __forceinline__ void skip_role(const ChainArgs& a, uint8_t* smem, int
           const int g = i * L + l, st = g & 1;
           mbar_wait(empty + st, ((uint32_t)(g >> 1) & 1) ^ 1);
           zring_consumed(a, p, g);
-          wait_counter(a.zflag + p, 2u * (uint32_t)(g + 1));
+          wait_counter(a.zflag + p, (uint32_t)a.zpub * (uint32_t)(g + 1));
           if (l == L - 1) trace_g(a, k == 0, 2);
           fence_proxy_async_all();
           uint8_t* stage = smem + st * kSkipStage;
@@ -383,6 +393,9 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
   uint64_t* a_free = bars + 15;    // block 1: block 0's image may take h (remote arrive)
   uint64_t* noise_ready = bars + 16;  // 128: Gumbel noise in TMEM [256,512)
   uint64_t* acc_init = bars + 17;     // 256: TMEM [0,256) holds the bias of s (next skip sum)
+  // block 0: block 1 has consumed block 0's s half (its head1 is complete), so block 0 may
+  // overwrite that half of its image -- the source of its outgoing s copy -- with h
+  uint64_t* s_free = bars + 18;
   uint8_t* img = smem;                 // [8 K-chunks][16 KB]: s, then (block 0) h
   uint8_t* wring = smem + kImgBytes;   // kWStages x 32 KB
   float* xch = reinterpret_cast<float*>(wring);
@@ -398,6 +411,7 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
     mbar_init(a_free, 1);
     mbar_init(noise_ready, 128);
     mbar_init(acc_init, 256);
+    mbar_init(s_free, 1);
     fence_mbar_init();
     mbar_arrive_expect_tx(peer_full, half_bytes);  // armed before the peer can send
   }
@@ -441,7 +455,7 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
           const uint8_t* wsrc = a.wskip2 + ((size_t)e * L + l) * 65536;
           mbar_arrive_expect_tx(full + st, 2 * kTile + 65536);
           if (l >= 2) bulk_g2s(stage + 2 * kTile, wsrc, 65536, full + st);
-          wait_counter(a.zflag + p, 2u * (uint32_t)(g + 1));
+          wait_counter(a.zflag + p, (uint32_t)a.zpub * (uint32_t)(g + 1));
           if (l == L - 1) trace_g(a, k == 0, 2);
           if (l < 2) bulk_g2s(stage + 2 * kTile, wsrc, 65536, full + st);
           fence_proxy_async_all();
@@ -577,6 +591,10 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
       if (sel_block) {
         // block 1 may now overwrite chunks 4..7 of this image with its half of h
         if (warp == 2 && lane == 0) mbar_arrive_remote(mapa(a_free, peer));
+        // the outgoing copy of this block's s half (chunks 0..3, about to take h) has landed
+        // in block 1 and been consumed by its head1 (a DSMEM bulk copy's source read is only
+        // known complete through the receiver)
+        mbar_wait_cluster(s_free, (uint32_t)i & 1);
         own_half(hbias);
         trace_g(a, k == 0 && warp == 2 && lane == 0, 4);
         mbar_wait(tacc, 1);  // head2 (2i+1 & 1)
@@ -600,8 +618,11 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
         if (i + 1 < a.n_steps) init_acc();
         trace_g(a, t2, 25);
       } else {
-        own_half(hbias);  // h columns 256..511 into this image's chunks 4..7
+        // block 0's head1 is complete, so this block's outgoing s copy (chunks 4..7, about
+        // to take h) has landed there; and this block's head1 has consumed block 0's s half
+        if (warp == 2 && lane == 0) mbar_arrive_remote(mapa(s_free, peer));
         mbar_wait_cluster(a_free, (uint32_t)i & 1);
+        own_half(hbias);  // h columns 256..511 into this image's chunks 4..7
         send_half();  // (before init_acc: block 0's head2 waits for this half of h)
         if (i + 1 < a.n_steps) init_acc();
       }
@@ -689,14 +710,23 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
   uint64_t* z1_ready = bars + 16;  // 256
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
   uint64_t* xd_free = bars + 18;   // commit: this layer's x_{t-d} MMAs are done with TMEM xd
-  uint64_t* z_stashed = bars + 21;  // 128: queue warps' z stash stores of this layer issued
+  uint64_t* z_stashed = bars + 21;  // 128: queue warps' z of this layer staged (or stored)
+  uint64_t* stage_free = bars + 19;  // [2] publisher: the z staging image's bulk store is done
   uint64_t* probe = bars + 24;      // [6] trace only: commits after MMA groups (warp 14 stamps)
   const bool tracing = a.trace != nullptr && blockIdx.x == 0;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int tile = blockIdx.x;
+  // split mode: the two CTAs of a cluster share one 64-stream tile, CTA `half` computing the
+  // dilated N-half `half` (its z columns 64 half .. +63); both keep the full residual stream
+  const bool split = a.split != 0;
+  const int tile = split ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
+  const int half = split ? (int)(blockIdx.x & 1) : 0;
   const int L = a.L;
   const int G = a.n_steps * L;  // layers of all steps of this launch, in order
+  // split: the peer's z half lands here (2 layer-parity buffers of [8 K-pieces][64 rows][16 B]
+  // in the unused A1 stage), completing zpeer[parity]'s transaction count
+  uint8_t* zpeer_buf = smem + kOffA1;
+  uint64_t* zpeer = bars + 30;  // [2]
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 11; ++i) mbar_init(bars + i, 1);
@@ -709,16 +739,40 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     mbar_init(xd_free, 1);
     mbar_init(z_stashed, 128);
     for (int i = 0; i < 6; ++i) mbar_init(probe + i, 1);
+    mbar_init(zpeer + 0, 1);
+    mbar_init(zpeer + 1, 1);
+    mbar_init(stage_free + 0, 1);
+    mbar_init(stage_free + 1, 1);
     fence_mbar_init();
   }
   if (warp == 1) tmem_alloc(tmem_holder, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (split) cluster_sync();  // both halves' barriers exist before any z crosses
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 0) {
-    if (lane == 0) {  // ---- weight producer ----
+    if (lane == 0 && split) {  // ---- weight producer, split: A_half | B_half | C ----
+      int gc = 0;
+      for (int g = 0; g < G; ++g) {
+        const int l = g % L;
+        const uint8_t* wl = a.w + (size_t)l * kLayerBytes;
+        const uint32_t ph = ((uint32_t)g & 1) ^ 1;
+        mbar_wait(emptyA0, ph);
+        mbar_arrive_expect_tx(fullA0, kStageA);
+        bulk_g2s(stA0, wl + half * kStageA, kStageA, fullA0);
+        mbar_wait(emptyB, ph);
+        mbar_arrive_expect_tx(fullB, kStageB / 2);
+        bulk_g2s(stB, wl + 2 * kStageA + half * (kStageB / 2), kStageB / 2, fullB);
+        if (l + 1 < L) {
+          mbar_wait(emptyC, ((uint32_t)gc & 1) ^ 1);
+          mbar_arrive_expect_tx(fullC, kStageC);
+          bulk_g2s(stC, wl + 2 * kStageA + kStageB, kStageC, fullC);
+          ++gc;
+        }
+      }
+    } else if (lane == 0) {  // ---- weight producer ----
       int gc = 0;  // res stages loaded (all but each step's top layer)
       for (int g = 0; g < G; ++g) {
         const int l = g % L;
@@ -743,6 +797,101 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
           bulk_g2s(stC, wl + 2 * kStageA + kStageB, kStageC, fullC);
           ++gc;
         }
+      }
+    }
+  } else if (warp == 1 && split) {  // ---- MMA issuer, split mode: one N-half ----
+    const uint32_t id = idesc_f16(kChainRows, 128);
+    const uint32_t sa0 = smem_u32(stA0), sb = smem_u32(stB), sc = smem_u32(stC),
+                   zp = smem_u32(zpeer_buf);
+    auto mma_tmem_a = [&](uint32_t d, uint32_t a_col, uint32_t b_saddr) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk)
+        mma_bf16_ta(d, a_col + kk * 8, sdesc_sw128(b_saddr + kk * 32), id, 1u);
+    };
+    // x_{t-d} taps of this half: initialise acc0 (stage A0), then free the operand
+    auto xd_mma = [&]() {
+#pragma unroll
+      for (int c = 0; c < 2; ++c)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          mma_bf16_ta(tmem, tmem + kColXd + 32 * c + 8 * kk, sdesc_sw128(sa0 + c * kChunk + kk * 32),
+                      id, (c | kk) ? 1u : 0u);
+      mma_commit(emptyA0);
+      mma_commit(xd_free);
+    };
+    bool early = false;
+    int gc = 0;
+    for (int g = 0; g < G; ++g) {
+      const int l = g % L;
+      const uint32_t par = (uint32_t)g & 1;
+      const bool nx = l + 1 < L, nxg = g + 1 < G;
+      if (!early) {
+        mbar_wait(xd_ready, par);
+        tc_fence_after();
+        mbar_wait(fullA0, par);
+        tc_fence_after();
+        if (elect_one()) xd_mma();
+        __syncwarp();
+      }
+      early = false;
+      mbar_wait(xt_ready, par);
+      tc_fence_after();
+      mbar_wait(fullB, par);
+      tc_fence_after();
+      if (elect_one()) {
+        mma_tmem_a(tmem, tmem + kColXt + 0, sb + 0 * kChunk);
+        mma_tmem_a(tmem, tmem + kColXt + 32, sb + 1 * kChunk);
+      }
+      __syncwarp();
+      if (g > 0) mbar_wait(z_read, par ^ 1);  // the previous layer's stash has read z
+      if (elect_one()) {
+        mma_commit(acc0_full);
+        mma_commit(emptyB);
+      }
+      __syncwarp();
+      // own z half (TMEM) -> residual K-chunk `half`
+      mbar_wait(z0_ready, par);
+      tc_fence_after();
+      if (nx) {
+        mbar_wait(fullC, (uint32_t)gc & 1);
+        tc_fence_after();
+        if (elect_one()) mma_tmem_a(tmem + kP1 + kColX, tmem + kP1 + kColZ + 32 * half, sc + half * kChunk);
+        __syncwarp();
+      }
+      // acc0 was read by the gate: the next layer's x_{t-d} (the next step's layer 0 too)
+      if (nxg) {
+        mbar_wait(xd_ready, par ^ 1);
+        tc_fence_after();
+        mbar_wait(fullA0, par ^ 1);
+        tc_fence_after();
+        if (elect_one()) xd_mma();
+        __syncwarp();
+        early = true;
+      }
+      // the peer's z half (SMEM, bulk-copied through DSMEM) -> residual K-chunk 1 - half
+      const int zb = g & 1;
+      if (elect_one()) mbar_arrive_expect_tx(zpeer + zb, 8192);
+      __syncwarp();
+      // cluster-scope acquire: the peer's st.async writes complete on this barrier with
+      // cluster-scope release; then the proxy fence orders them (generic proxy) before this
+      // thread's MMA reads (async proxy)
+      mbar_wait_cluster(zpeer + zb, (uint32_t)(g >> 1) & 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_after();
+      if (nx) {
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)  // K = 16 (2 pieces) per MMA, half h = kk / 2
+            mma_bf16(tmem + kP1 + kColX,
+                     sdesc_plain(zp + zb * 8192 + (kk >> 1) * 4096 + (kk & 1) * 256, 128, 512),
+                     sdesc_sw128(sc + (1 - half) * kChunk + kk * 32), id, 1u);
+          mma_commit(emptyC);
+        }
+        __syncwarp();
+        mbar_wait(x_pushed, par);
+        if (elect_one()) mma_commit(x_full);
+        __syncwarp();
+        ++gc;
       }
     }
   } else if (warp == 1) {  // ---- MMA issuer (whole warp; MMAs under elect.sync) ----
@@ -933,9 +1082,12 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
     };
     // 64 TMEM columns of packed fp16 pairs (32x32b: lanes 0..15 read P0, 16..31 read P1)
     // -> 16 K-pieces at dst (+ j * stride rows) from the lanes with `mine`
+    // (split: only the 16-column groups c of this CTA's half; the peer does the others)
+    const int c_lo = split ? 2 * half : 0, c_hi = split ? 2 * half + 2 : 4;
     auto tmem_to_pieces = [&](uint32_t col, uint4* dst, int stride, bool mine) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
+        if (c < c_lo || c >= c_hi) continue;
         float v[16];
         tmem_ld16(trow + col + 16 * c, v);
         tmem_wait_ld();
@@ -987,26 +1139,54 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
         }
         __syncwarp();
       }
-      mbar_wait(z1_ready, par);
+      mbar_wait(split ? z0_ready : z1_ready, par);
       tc_fence_after();
-      tmem_to_pieces(kColZ, zstash_rows(a.zimg, tile, a.zring, g % a.zring) + r, 2 * kChainRows, !act);
+      if (a.zflag != nullptr) {
+        // fused: z into a shared-memory staging image; the publisher bulk-stores it into the
+        // stash, waits for the store's completion and only then releases the counter the
+        // tail blocks acquire (per-thread global stores published by another warp's release
+        // were seen stale by the tail now and then: the release covers only its own warp)
+        if (g >= 2) mbar_wait(stage_free + (g & 1), (uint32_t)(((g >> 1) - 1) & 1));
+        tmem_to_pieces(kColZ, reinterpret_cast<uint4*>(smem + kOffZs + (g & 1) * kSlotBytes) + r,
+                       kChainRows, !act);
+        fence_proxy_async();  // generic shared writes -> the bulk store (async proxy)
+      } else {
+        tmem_to_pieces(kColZ, zstash_rows(a.zimg, tile, a.zring, g % a.zring) + r, 2 * kChainRows, !act);
+      }
       tc_fence_before();
       mbar_arrive(z_read);
-      mbar_arrive(z_stashed);  // warp 14 publishes them (its release fence waits on the stores)
+      mbar_arrive(z_stashed);
       if (tq) trace_at(a, l, T_SP2, clock64());
       if (tq) trace_at(a, l, T_SP1, clock64());
       if (tq) trace_at(a, l, T_SP3, clock64());
     }
   } else if (warp == 14) {
     // ---- publisher: z_l of this tile -> the tail blocks (release of the stash stores) ----
-    if (lane == 0 && a.zflag != nullptr) {
+    if (a.zflag != nullptr) {
+      // one K-piece (1 KB) per lane: a thread's bulk copies run one after another, several
+      // threads' overlap
+      const int j0 = split ? 8 * half : 0, j1 = split ? 8 * half + 8 : 16;  // K-pieces
+      const int j = j0 + lane;
       for (int g = 0; g < G; ++g) {
         mbar_wait(z_stashed, (uint32_t)g & 1);
-        red_release_gpu(a.zflag + (tile >> 1), 1u);
+        if (j < j1) {
+          const uint8_t* src = smem + kOffZs + (g & 1) * kSlotBytes;
+          uint8_t* dst = reinterpret_cast<uint8_t*>(zstash_rows(a.zimg, tile, a.zring, g % a.zring));
+          bulk_s2g(dst + j * 2048, src + j * 1024, 1024);
+          bulk_commit();
+          bulk_wait0();             // this piece is in the stash
+          fence_proxy_async_all();  // async-proxy writes before the release below
+        }
+        __syncwarp();
+        if (lane == 0) {
+          red_release_gpu(a.zflag + (tile >> 1), 1u);
+          mbar_arrive(stage_free + (g & 1));
+        }
+        __syncwarp();
       }
     }
   } else if (warp == 15) {
-    if (lane == 0 && tracing) {
+    if (lane == 0 && tracing && !split) {  // (the split MMA issuer commits no probes)
       // trace: completion times of the MMA groups (probe commits, in pipe order)
       for (int g = 0; g < G; ++g)
         for (int k = 0; k < 6; ++k) {
@@ -1095,10 +1275,13 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
       mbar_arrive(xt_ready);
       if (tr) trace_at(a, l, T_EPI_XT, clock64());
       if (l == 0) trace_g(a, tr, 18);
-      // gate of N-half hh: this lane's 16 z columns 64hh + 32h + 2j + pc, j < 16
+      // gate of N-half hh: this lane's 16 z columns 64hh + 32h + 2j + pc, j < 16 (split: the
+      // CTA's one half, accumulated in acc0)
       const float* bd = a.dil_b + (size_t)l * 2 * kD;
 #pragma unroll
       for (int hh = 0; hh < 2; ++hh) {
+        if (split && hh > 0) break;
+        const int zh = split ? half : hh;  // the z columns' half
         mbar_wait(hh == 0 ? acc0_full : acc1_full, par);
         if (tr) trace_at(a, l, hh == 0 ? T_EPI_ACC0 : T_EPI_ACC1, clock64());
         tc_fence_after();
@@ -1112,7 +1295,7 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
           as[j] = __uint_as_float(ts[16 + j]);
         }
         if (a.has_dil_bias) {
-          const int j0 = 64 * hh + 32 * h + pc;
+          const int j0 = 64 * zh + 32 * h + pc;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             at[j] += __ldg(bd + j0 + 2 * j);
@@ -1129,11 +1312,51 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
           asm volatile("" ::"r"(zw[0]), "r"(zw[7]) : "memory");
           trace_at(a, l, hh == 0 ? T_G0_MATH : T_G1_MATH, clock64());
         }
-        tmem_st_16x64b_x8(trow + kP1 + kColZ + 32 * hh + 16 * h, zw);
+        tmem_st_16x64b_x8(trow + kP1 + kColZ + 32 * zh + 16 * h, zw);
         tmem_wait_st();
         tc_fence_before();
         mbar_arrive(hh == 0 ? z0_ready : z1_ready);
-        if (tr) trace_at(a, l, hh == 0 ? T_EPI_Z0 : T_EPI_Z1, clock64());
+        if (split) {
+          // this half's z -> the peer's residual K-chunk: 16-byte K-pieces (8 z columns of
+          // one row) stored straight into the peer's operand image [h][8-row group][4 pieces]
+          // [8 rows][16 B] (K-adjacent core matrices 128 B apart, 8-row groups 512 B apart)
+          // by st.async, each completing 16 bytes of the peer's zpeer transaction count -- no
+          // staging, no barrier across the gate warps, no bulk-copy queue. Piece m of this
+          // lane group (z columns 32h + 8m .. +7) = packed columns 4m .. 4m+3, held
+          // alternately by this lane (parity pc) and its partner t ^ 2.
+          uint32_t pw[8];
+#pragma unroll
+          for (int i = 0; i < 8; ++i) pw[i] = __shfl_xor_sync(0xffffffffu, zw[i], 2);
+          const int zb = g & 1;
+          const int rg = row >> 3, r8 = row & 7;  // 8-row group, row inside it
+          const uint32_t zbar = mapa(zpeer + zb, (uint32_t)(half ^ 1));
+          uint8_t* stage = smem + kOffB + 32768 + zb * 8192;  // (stage B's unused half)
+#pragma unroll
+          for (int mm = 0; mm < 2; ++mm) {
+            const int m = 2 * pc + mm;
+            const uint32_t lo0 = pc == 0 ? zw[2 * m] : pw[2 * m], hi0 = pc == 0 ? pw[2 * m] : zw[2 * m];
+            const uint32_t lo1 = pc == 0 ? zw[2 * m + 1] : pw[2 * m + 1],
+                           hi1 = pc == 0 ? pw[2 * m + 1] : zw[2 * m + 1];
+            const uint32_t off = (uint32_t)(h * 4096 + rg * 512 + m * 128 + r8 * 16);
+            if (kSplitBulk) {
+              st_shared_v4(smem_u32(stage + off), lo0, hi0, lo1, hi1);
+            } else {
+              asm volatile(
+                  "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(
+                      mapa(zpeer_buf + zb * 8192 + off, (uint32_t)(half ^ 1))),
+                  "r"(lo0), "r"(hi0), "r"(lo1), "r"(hi1), "r"(zbar)
+                  : "memory");
+            }
+          }
+          if (kSplitBulk) {  // the warp's 16 rows x 4 pieces: one contiguous 1 KB block
+            fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) {
+              const uint32_t off = (uint32_t)(h * 4096 + q * 1024);
+              bulk_s2peer(mapa(zpeer_buf + zb * 8192 + off, (uint32_t)(half ^ 1)), stage + off, 1024, zbar);
+            }
+          }
+        }
       }
       if (l == L - 1) trace_g(a, tr, 1);
     }
@@ -1141,5 +1364,6 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (split) cluster_sync();  // no DSMEM copy into a CTA that has exited
   if (warp == 1) tmem_dealloc(tmem, 512);
 }

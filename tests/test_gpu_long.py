@@ -144,3 +144,35 @@ def test_cfg2_full_1000_steps(cuda, L):
     ties = check_streams(oc.CellOracle(m, exact=False), np.array([[128]]), out, lg, [0],
                          configs.SAMPLE_INVCDF, configs.NOISE_SEED, 1e-4, 1e-5, report=report)
     assert ties <= 2, report
+
+
+@pytest.mark.parametrize("B", [512, 1152])
+def test_cfg4_split_chain_matches_unsplit_and_oracle(cuda, cfg4_model, monkeypatch, B):
+    """Batches whose tiles fit twice on the SMs run each 64-stream tile over a 2-CTA cluster
+    (one dilated N-half per CTA, z halves exchanged through DSMEM, the residual accumulated
+    in both). 600 teacher-forced steps (past the d = 512 ring wrap): every stream's logits
+    against the unsplit kernel, a few against the oracle, and the folded-tail Gumbel free
+    run choice by choice."""
+    n = 600
+    cls = np.random.default_rng(B).integers(0, 256, (n, B)).astype(np.int32)
+    gen = CellGenerator(cfg4_model, B, kernel="tcgen05")
+    streams = [0, 63, 64, 200, B - 1]
+    out, lg, lg_split = _run(gen, cls, n, Sampler(0), n, streams)
+    gen.close()
+    report = []
+    check_streams(oc.CellOracle(cfg4_model, exact=False), cls[:, streams], out[:, streams], lg,
+                  range(len(streams)), 0, 0, 2e-2, 4e-2, report=report, gids=streams)
+    monkeypatch.setenv("FW_CHAIN_SPLIT", "0")
+    ref = CellGenerator(cfg4_model, B, kernel="tcgen05")
+    _, _, lg_ref = _run(ref, cls, n, Sampler(0), n, streams)
+    ref.close()
+    dev = max(float((lg_split[t:t + 100] - lg_ref[t:t + 100]).abs().max()) for t in range(0, n, 100))
+    assert dev <= 2e-2, dev
+    monkeypatch.delenv("FW_CHAIN_SPLIT")
+    gen = CellGenerator(cfg4_model, B, kernel="tcgen05")
+    primer = np.full((1, B), 128)
+    free, _, _ = _run(gen, primer, 300, Sampler(configs.SAMPLE_GUMBEL, configs.NOISE_SEED), 0, streams)
+    gen.close()
+    check_streams(oc.CellOracle(cfg4_model, exact=False), primer[:, streams], free[:, streams], None,
+                  range(len(streams)), configs.SAMPLE_GUMBEL, configs.NOISE_SEED, 2e-2, 4e-2,
+                  gids=streams)

@@ -33,14 +33,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="cfg4")
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--batch", type=int, default=0)
     args = ap.parse_args()
     spec = configs.by_name(args.config)
     m = build_cell_model(spec.cell)
-    gen = CellGenerator(m, spec.batch, kernel="tcgen05")
+    B = args.batch or spec.batch
+    gen = CellGenerator(m, B, kernel="tcgen05")
     L = spec.cell.total_layers
     tr = torch.zeros((L + 1, SLOTS), dtype=torch.int64, device="cuda")
     _lib.check(gen._lib.fw_debug_trace(gen._h, C.c_void_p(tr.data_ptr())))
-    primer = torch.full((1, spec.batch), 128, dtype=torch.int32, device="cuda")
+    primer = torch.full((1, B), 128, dtype=torch.int32, device="cuda")
     gen.generate(primer, args.steps, Sampler(spec.sampler, configs.NOISE_SEED))
     torch.cuda.synchronize()
     t = tr.cpu().numpy().astype(np.int64)
