@@ -176,3 +176,54 @@ def test_cfg4_split_chain_matches_unsplit_and_oracle(cuda, cfg4_model, monkeypat
     check_streams(oc.CellOracle(cfg4_model, exact=False), primer[:, streams], free[:, streams], None,
                   range(len(streams)), configs.SAMPLE_GUMBEL, configs.NOISE_SEED, 2e-2, 4e-2,
                   gids=streams)
+
+
+@pytest.mark.parametrize("B,split", [(2048, "1"), (2048, "0"), (4096, "1")])
+def test_tcgen05_repeated_runs_are_bit_identical(cuda, cfg4_model, monkeypatch, B, split):
+    """Race detector: the persistent step kernel's warps, tiles and tail blocks hand data to
+    each other through mbarriers, DSMEM and global counters; a missing ordering edge shows up
+    as an occasional step whose logits differ between identical runs (this found the z-stash
+    publication and the pair tail's image reuse). Four identical 600-step teacher-forced
+    runs must agree bit for bit."""
+    monkeypatch.setenv("FW_CHAIN_SPLIT", split)
+    n = 600
+    cls = torch.as_tensor(np.random.default_rng(B + 7).integers(0, 256, (n, B)), dtype=torch.int32,
+                          device="cuda")
+    ref = None
+    for _ in range(4):
+        gen = CellGenerator(cfg4_model, B, kernel="tcgen05")
+        _, lg = gen.generate(cls, n, Sampler(0), n_logit_steps=n)
+        torch.cuda.synchronize()
+        gen.close()
+        if ref is None:
+            ref = lg
+            continue
+        bad = torch.nonzero((lg - ref).abs().amax(dim=2) > 0)
+        assert bad.shape[0] == 0, bad[:8].tolist()
+        del lg
+
+
+@pytest.mark.parametrize("config,batch,cluster", [("cfg1", 1, ""), ("cfg2_L8", 2, "16"),
+                                                  ("cfg3", 64, ""), ("cfg5", 1024, "")])
+def test_simt_repeated_runs_are_bit_identical(cuda, monkeypatch, config, batch, cluster):
+    """Race detector for the fp32 kernels (the small-batch cluster kernel's st.async
+    exchanges and weight ring, the staged kernel's producer/consumer ring): three identical
+    teacher-forced runs, past the largest ring wrap where affordable, agree bit for bit."""
+    if cluster:
+        monkeypatch.setenv("FW_SIMT_CLUSTER", cluster)
+    spec = configs.by_name(config)
+    m = build_cell_model(spec.cell)
+    n = 300 if config == "cfg5" else 600
+    cls = torch.as_tensor(np.random.default_rng(3).integers(0, 256, (n, batch)), dtype=torch.int32,
+                          device="cuda")
+    ref = None
+    for _ in range(3):
+        gen = CellGenerator(m, batch, kernel="simt")
+        _, lg = gen.generate(cls, n, Sampler(0), n_logit_steps=n)
+        torch.cuda.synchronize()
+        gen.close()
+        if ref is None:
+            ref = lg
+            continue
+        bad = torch.nonzero((lg - ref).abs().amax(dim=2) > 0)
+        assert bad.shape[0] == 0, bad[:8].tolist()
