@@ -44,9 +44,36 @@ namespace {
 constexpr int kLatNT = 512;   // 16 warps: the phases are latency-bound, more lanes per GEMV
 constexpr int kLatPad = 128;  // zero floats after every input vector (padded GEMV rows)
 
-// Per-C packed weights and their layout (host-computed, uploaded once per handle and C).
-struct LatLayout {
-  int C = 0;
+constexpr int lat_pow2_floor(int v) {
+  int p = 1;
+  while (p * 2 <= v) p *= 2;
+  return p;
+}
+constexpr int lat_max(int a, int b) { return a > b ? a : b; }
+constexpr int lat_min(int a, int b) { return a < b ? a : b; }
+constexpr int64_t lat_max64(int64_t a, int64_t b) { return a > b ? a : b; }
+// lanes per output so that the n outputs fill `threads` (at most max_lpo)
+constexpr int lpo_for(int n, int max_lpo, int threads) {
+  return lat_max(1, lat_min(lat_pow2_floor(lat_max(1, threads / lat_max(n, 1))), max_lpo));
+}
+// row stride (floats): K rounded up to whole chunks of every lane of an output group
+// (4 lpo floats, at least 32), then offset so the 16-byte chunks a quarter-warp loads -- 8 / lpo
+// rows, lpo consecutive chunks each -- land in distinct bank groups
+constexpr int kpad(int K, int lpo) {
+  return lpo < 8 ? (K + lat_max(32, 4 * lpo) - 1) / lat_max(32, 4 * lpo) * lat_max(32, 4 * lpo) + 4 * lpo
+                 : (K + lat_max(32, 4 * lpo) - 1) / lat_max(32, 4 * lpo) * lat_max(32, 4 * lpo);
+}
+constexpr int64_t up4(int64_t v) { return (v + 3) & ~(int64_t)3; }  // 16-byte granules
+constexpr int lat_lg2(int v) {
+  int r = 0;
+  while ((1 << r) < v) ++r;
+  return r;
+}
+
+// Geometry of one rank's weight blocks for a shape (R, D, S, H, A) and cluster size C --
+// independent of L. Computed at compile time for the BASELINE shapes the kernel is
+// specialised for (the loops of the phases then unroll), at run time otherwise.
+struct LatGeom {
   int Dc, Rc, Sc, Hc, Ac;
   int Kd, Kpd, lpo_d;    // dil: K = 2R + D, padded row, lanes per output
   int Kprs, lpo_rs;      // res | skip rows over z (K = D)
@@ -58,10 +85,74 @@ struct LatLayout {
   int64_t post_floats;   // block L: skip rows + bias
   int64_t h1_floats, h2_floats;  // one head block: rows (h1r / h2r of the slice) + biases
   int h1p, h2p, h1r, h2r;          // head slices split into parts of at most h1r / h2r rows
-  int64_t step_floats;      // all blocks of a step (per rank)
   int64_t max_block;
+};
+
+constexpr LatGeom lat_geom(int R, int D, int S, int H, int A, int C) {
+  LatGeom g{};
+  g.Dc = D / C;
+  g.Rc = R / C;
+  g.Sc = S / C;
+  g.Hc = H / C;
+  g.Ac = A / C;
+  g.Kd = 2 * R + D;
+  g.lpo_d = lpo_for(2 * g.Dc, 16, kLatNT / 2);  // a z column's two rows in one warp
+  g.Kpd = kpad(g.Kd, g.lpo_d);
+  g.lpo_rs = lpo_for(g.Rc + g.Sc, 32, kLatNT / 2);
+  g.Kprs = kpad(D, g.lpo_rs);
+  g.lpo_h1 = lpo_for(g.Hc, 32, kLatNT);
+  g.Kph1 = kpad(S, g.lpo_h1);
+  g.lpo_h2 = lpo_for(g.Ac, 32, kLatNT);
+  g.Kph2 = kpad(H, g.lpo_h2);
+  g.lg_d = lat_lg2(g.lpo_d);
+  g.lg_rs = lat_lg2(g.lpo_rs);
+  g.lg_h1 = lat_lg2(g.lpo_h1);
+  g.lg_h2 = lat_lg2(g.lpo_h2);
+  g.o_dil = 0;
+  g.o_bd = up4((int64_t)2 * g.Dc * g.Kpd);
+  g.o_rs = g.o_bd + up4(2 * g.Dc);
+  g.o_br = g.o_rs + up4((int64_t)(g.Rc + g.Sc) * g.Kprs);
+  g.o_bs = g.o_br + up4(g.Rc);
+  g.phase_floats = g.o_bs + up4(g.Sc);
+  g.post_floats = up4((int64_t)g.Sc * g.Kprs) + up4(g.Sc);
+  // head slices in parts no larger than a phase block (the ring's slot size), so a config
+  // with wide heads and narrow layers (cfg3) still streams through two slots
+  const int64_t cap = lat_max64(g.phase_floats, g.post_floats);
+  g.h1r = g.Hc;
+  g.h1p = 1;
+  while (g.h1r > 1 && up4((int64_t)g.h1r * g.Kph1) + up4(g.h1r) > cap) g.h1r = (g.Hc + ++g.h1p - 1) / g.h1p;
+  g.h1p = (g.Hc + g.h1r - 1) / g.h1r;
+  g.h1_floats = up4((int64_t)g.h1r * g.Kph1) + up4(g.h1r);
+  g.h2r = g.Ac;
+  g.h2p = 1;
+  while (g.h2r > 1 && up4((int64_t)g.h2r * g.Kph2) + up4(g.h2r) > cap) g.h2r = (g.Ac + ++g.h2p - 1) / g.h2p;
+  g.h2p = (g.Ac + g.h2r - 1) / g.h2r;
+  g.h2_floats = up4((int64_t)g.h2r * g.Kph2) + up4(g.h2r);
+  g.max_block = lat_max64(lat_max64(g.phase_floats, g.post_floats), lat_max64(g.h1_floats, g.h2_floats));
+  return g;
+}
+
+// Per-C packed weights and their layout (host-computed, uploaded once per handle and C).
+struct LatLayout {
+  int C = 0;
+  LatGeom g{};
+  int64_t step_floats;      // all blocks of a step (per rank)
   int resident;
   float* d_w = nullptr;     // [C][step_floats]
+};
+
+// Compile-time shapes the kernel is specialised for (0: the generic kernel, shape at run
+// time): BASELINE configs 1, 2 and 3 at their cluster sizes.
+template <int R_, int D_, int S_, int H_, int A_, int C_>
+struct LatShape {
+  static constexpr bool kFixed = true;
+  static constexpr int R = R_, D = D_, S = S_, H = H_, A = A_;
+  static constexpr LatGeom G = lat_geom(R_, D_, S_, H_, A_, C_);
+};
+struct LatAnyShape {
+  static constexpr bool kFixed = false;
+  static constexpr int R = 0, D = 0, S = 0, H = 0, A = 0;
+  static constexpr LatGeom G{};
 };
 
 }  // namespace
@@ -227,12 +318,16 @@ __device__ __forceinline__ void lat_send(LatSeg a, LatSeg b, LatSeg c, uint64_t*
   }
 }
 
-template <int C>
+template <int C, class Sh>
 __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
   extern __shared__ __align__(16) float smem[];
   const CellDims d = p.d;
-  const LatLayout& Y = p.lay;
-  const int R = d.R, D = d.D, S = d.S, H = d.H, A = d.A, L = d.L;
+  const LatLayout& Yr = p.lay;
+  // the geometry: compile-time constants for a specialised shape (the phases' loops unroll)
+  const LatGeom Y = Sh::kFixed ? Sh::G : Yr.g;
+  const int R = Sh::kFixed ? Sh::R : d.R, D = Sh::kFixed ? Sh::D : d.D,
+            S = Sh::kFixed ? Sh::S : d.S, H = Sh::kFixed ? Sh::H : d.H,
+            A = Sh::kFixed ? Sh::A : d.A, L = d.L;
   const int Dc = Y.Dc, Rc = Y.Rc, Sc = Y.Sc, Hc = Y.Hc, Ac = Y.Ac;
   const uint32_t rank = lat_rank();
   const int stream = blockIdx.x / C;
@@ -243,7 +338,7 @@ __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
   // staged slices (z, x, x_{t-d}, ReLU(s), h, logits) | s[Sc] | sf[S + pad] | hf[H + pad] |
   // lg[A] | cls
   float* wsm = smem;
-  const int64_t wfl = Y.resident ? Y.step_floats : 2 * Y.max_block;
+  const int64_t wfl = Yr.resident ? Yr.step_floats : 2 * Y.max_block;
   const int in_len = (2 * R + D + kLatPad + 3) & ~3;
   uint64_t* full = reinterpret_cast<uint64_t*>(wsm + wfl);  // [2] weight ring slots
   uint64_t* xbar = full + 2;                                  // [2] exchanges (alternating)
@@ -261,7 +356,7 @@ __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
   int* cls = reinterpret_cast<int*>(lg + A);
   // this step's ring slot base (element offset) of every layer, + layer 0's of the next step
   int64_t* rslot = reinterpret_cast<int64_t*>((reinterpret_cast<uintptr_t>(cls + 4) + 7) & ~(uintptr_t)7);
-  const float* wg = p.w + (int64_t)rank * Y.step_floats;  // this rank's blocks in global
+  const float* wg = p.w + (int64_t)rank * Yr.step_floats;  // this rank's blocks in global
   // blocks of a step: L phases, the top skip, h1p parts of head1, h2p parts of head2
   const int nblk = L + 1 + Y.h1p + Y.h2p;
   auto block_off = [&](int b) -> int64_t {  // float offset of block b inside a step
@@ -310,8 +405,8 @@ __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
     ptx::bulk_g2s(wsm + (gi & 1) * Y.max_block, wg + block_off(b), bytes, &full[gi & 1]);
   };
   if (tid == ctl) {
-    if (Y.resident) {
-      const uint32_t bytes = (uint32_t)(Y.step_floats * 4);
+    if (Yr.resident) {
+      const uint32_t bytes = (uint32_t)(Yr.step_floats * 4);
       ptx::mbar_arrive_expect_tx(&full[0], bytes);
       ptx::bulk_g2s(wsm, wg, bytes, &full[0]);
     } else {
@@ -321,14 +416,14 @@ __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
   // block b of the current step, waited for; the next block's copy goes into the slot the
   // previous phase released (every phase ends with a CTA barrier before its sends)
   auto take = [&](int b) -> const float* {
-    if (Y.resident) return wsm + block_off(b);
+    if (Yr.resident) return wsm + block_off(b);
     ptx::mbar_wait(&full[g & 1], (uint32_t)((g >> 1) & 1));
     const float* w = wsm + (g & 1) * Y.max_block;
     if (tid == ctl && g + 1 < (int64_t)run.n_steps * nblk) issue(g + 1);
     ++g;
     return w;
   };
-  if (Y.resident) ptx::mbar_wait(&full[0], 0);
+  if (Yr.resident) ptx::mbar_wait(&full[0], 0);
   // exchange e of the launch completes on xbar[e & 1]; this CTA arms it with the bytes it
   // will receive (transactions that arrive first drive the count negative until then)
   int64_t ex = 0;
@@ -491,30 +586,9 @@ __global__ void __launch_bounds__(kLatNT) cell_lat_kernel(LatParams p) {
   lat_cluster_sync();  // no remote stores into a CTA that has exited
 }
 
-int pow2_floor(int v) {
-  int p = 1;
-  while (p * 2 <= v) p *= 2;
-  return p;
-}
-// lanes per output so that the n outputs fill the CTA's 8 warps (at least 2 outputs per warp
-// when pairs must share a warp)
-int lpo_for(int n, int max_lpo, int threads = kLatNT) {
-  int lpo = pow2_floor(std::max(1, threads / std::max(n, 1)));
-  return std::max(1, std::min(lpo, max_lpo));
-}
-// row stride (floats): K rounded up to whole chunks of every lane of an output group
-// (4 lpo floats, at least 32), then offset so the 16-byte chunks a quarter-warp loads -- 8 / lpo
-// rows, lpo consecutive chunks each -- land in distinct bank groups
-int kpad(int K, int lpo) {
-  const int q = std::max(32, 4 * lpo);
-  const int kr = (K + q - 1) / q * q;
-  return lpo < 8 ? kr + 4 * lpo : kr;
-}
-int64_t up4(int64_t v) { return (v + 3) & ~(int64_t)3; }  // 16-byte granules
-
 // shared memory beside the weights (floats): barriers, inbuf, staged slices, s, sf, hf,
 // lg, cls -- the kernel's carve-up
-int64_t lat_act_floats(const CellDims& d, const LatLayout& Y) {
+int64_t lat_act_floats(const CellDims& d, const LatGeom& Y) {
   const int64_t stg = up4(std::max(std::max(Y.Dc + 2 * Y.Rc, Y.Sc + Y.Rc), std::max(Y.Hc, Y.Ac)));
   return 8 + 2 * up4(2 * d.R + d.D + kLatPad) + 2 * stg + up4(Y.Sc) + up4(d.S + kLatPad) + up4(d.H + kLatPad) +
          d.A + 4 + 2 * (d.L + 1) + 2;
@@ -544,71 +618,27 @@ static int lat_prepare(Handle& h, int C, std::string* err) {
   const CellDims& d = h.dims;
   const int L = d.L, R = d.R, D = d.D, S = d.S, H = d.H, A = d.A;
   const HostCell& w = h.host;
-  LatLayout Y;
-  Y.C = C;
-  Y.Dc = D / C;
-  Y.Rc = R / C;
-  Y.Sc = S / C;
-  Y.Hc = H / C;
-  Y.Ac = A / C;
-  Y.Kd = 2 * R + D;
-  Y.lpo_d = lpo_for(2 * Y.Dc, 16, kLatNT / 2);  // a z column's two rows in one warp
-  Y.Kpd = kpad(Y.Kd, Y.lpo_d);
-  Y.lpo_rs = lpo_for(Y.Rc + Y.Sc, 32, kLatNT / 2);
-  Y.Kprs = kpad(D, Y.lpo_rs);
-  Y.lpo_h1 = lpo_for(Y.Hc, 32);
-  Y.Kph1 = kpad(S, Y.lpo_h1);
-  Y.lpo_h2 = lpo_for(Y.Ac, 32);
-  Y.Kph2 = kpad(H, Y.lpo_h2);
-  auto lg2 = [](int v) {
-    int r = 0;
-    while ((1 << r) < v) ++r;
-    return r;
-  };
-  Y.lg_d = lg2(Y.lpo_d);
-  Y.lg_rs = lg2(Y.lpo_rs);
-  Y.lg_h1 = lg2(Y.lpo_h1);
-  Y.lg_h2 = lg2(Y.lpo_h2);
-  Y.o_dil = 0;
-  Y.o_bd = up4((int64_t)2 * Y.Dc * Y.Kpd);
-  Y.o_rs = Y.o_bd + up4(2 * Y.Dc);
-  Y.o_br = Y.o_rs + up4((int64_t)(Y.Rc + Y.Sc) * Y.Kprs);
-  Y.o_bs = Y.o_br + up4(Y.Rc);
-  Y.phase_floats = Y.o_bs + up4(Y.Sc);
-  Y.post_floats = up4((int64_t)Y.Sc * Y.Kprs) + up4(Y.Sc);
-  // head slices in parts no larger than a phase block (the ring's slot size), so a config
-  // with wide heads and narrow layers (cfg3) still streams through two slots
-  const int64_t cap = std::max(Y.phase_floats, Y.post_floats);
-  auto parts = [&](int rows, int Kp, int* np, int* rpp, int64_t* fl) {
-    *np = 1;
-    *rpp = rows;
-    while (*rpp > 1 && up4((int64_t)*rpp * Kp) + up4(*rpp) > cap) {
-      ++*np;
-      *rpp = (rows + *np - 1) / *np;
-    }
-    *np = (rows + *rpp - 1) / *rpp;
-    *fl = up4((int64_t)*rpp * Kp) + up4(*rpp);
-  };
-  parts(Y.Hc, Y.Kph1, &Y.h1p, &Y.h1r, &Y.h1_floats);
-  parts(Y.Ac, Y.Kph2, &Y.h2p, &Y.h2r, &Y.h2_floats);
-  Y.step_floats = (int64_t)L * Y.phase_floats + Y.post_floats + Y.h1p * Y.h1_floats + Y.h2p * Y.h2_floats;
-  Y.max_block = std::max(std::max(Y.phase_floats, Y.post_floats), std::max(Y.h1_floats, Y.h2_floats));
+  LatLayout Yl;
+  Yl.C = C;
+  Yl.g = lat_geom(R, D, S, H, A, C);
+  const LatGeom& Y = Yl.g;
+  Yl.step_floats = (int64_t)L * Y.phase_floats + Y.post_floats + Y.h1p * Y.h1_floats + Y.h2p * Y.h2_floats;
   // activations + barriers beside the weights; resident when a step's blocks fit
   const int64_t act_floats = lat_act_floats(d, Y);
   const int64_t budget = 220 * 1024 / 4;
-  Y.resident = (Y.step_floats + act_floats <= budget && Y.step_floats * 4 < (1u << 20)) ? 1 : 0;
-  if (!Y.resident && 2 * Y.max_block + act_floats > budget) {
+  Yl.resident = (Yl.step_floats + act_floats <= budget && Yl.step_floats * 4 < (1u << 20)) ? 1 : 0;
+  if (!Yl.resident && 2 * Y.max_block + act_floats > budget) {
     *err = "small-batch cluster kernel: a phase's weight slices exceed shared memory";
     return FW_ERR_UNSUPPORTED;
   }
-  std::vector<float> img((size_t)C * Y.step_floats, 0.f);
+  std::vector<float> img((size_t)C * Yl.step_floats, 0.f);
   // [l][o][k] accessors of the host model (reference layouts)
   auto W0 = [&](int l, int o, int k) { return (double)w.dil_w[(((size_t)l * 2 + 0) * 2 * D + o) * R + k]; };
   auto W1 = [&](int l, int o, int k) { return (double)w.dil_w[(((size_t)l * 2 + 1) * 2 * D + o) * R + k]; };
   auto Wr = [&](int l, int r, int k) { return (double)w.res_w[((size_t)l * R + r) * D + k]; };
   auto Ws = [&](int l, int s, int k) { return (double)w.skip_w[((size_t)l * S + s) * D + k]; };
   for (int q = 0; q < C; ++q) {
-    float* base = img.data() + (size_t)q * Y.step_floats;
+    float* base = img.data() + (size_t)q * Yl.step_floats;
     for (int l = 0; l < L; ++l) {
       float* blk = base + (size_t)l * Y.phase_floats;
       for (int j = 0; j < Y.Dc; ++j)
@@ -662,29 +692,29 @@ static int lat_prepare(Handle& h, int C, std::string* err) {
       part[(int64_t)Y.h2r * Y.Kph2 + ro] = w.h2_b[q * Y.Ac + o];
     }
   }
-  cudaError_t e = cudaMalloc(&Y.d_w, sizeof(float) * img.size());
-  if (e == cudaSuccess) e = cudaMemcpy(Y.d_w, img.data(), sizeof(float) * img.size(), cudaMemcpyHostToDevice);
+  cudaError_t e = cudaMalloc(&Yl.d_w, sizeof(float) * img.size());
+  if (e == cudaSuccess) e = cudaMemcpy(Yl.d_w, img.data(), sizeof(float) * img.size(), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
-    if (Y.d_w) cudaFree(Y.d_w);
+    if (Yl.d_w) cudaFree(Yl.d_w);
     *err = std::string("small-batch cluster kernel weights: ") + cudaGetErrorString(e);
     return FW_ERR_CUDA;
   }
-  h.lat = new LatPlan{Y};
+  h.lat = new LatPlan{Yl};
   return FW_OK;
 }
 
 static size_t lat_smem_bytes(const CellDims& d, const LatLayout& Y) {
-  const int64_t wfl = Y.resident ? Y.step_floats : 2 * Y.max_block;
-  return sizeof(float) * (size_t)(wfl + lat_act_floats(d, Y)) + 16;
+  const int64_t wfl = Y.resident ? Y.step_floats : 2 * Y.g.max_block;
+  return sizeof(float) * (size_t)(wfl + lat_act_floats(d, Y.g)) + 16;
 }
 
-template <int C>
+template <int C, class Sh>
 static cudaError_t lat_launch(const LatParams& p, size_t smem, cudaStream_t st) {
-  cudaError_t e = cudaFuncSetAttribute(cell_lat_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  cudaError_t e = cudaFuncSetAttribute(cell_lat_kernel<C, Sh>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   if (C > 8) {
-    e = cudaFuncSetAttribute(cell_lat_kernel<C>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    e = cudaFuncSetAttribute(cell_lat_kernel<C, Sh>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg{};
@@ -700,7 +730,7 @@ static cudaError_t lat_launch(const LatParams& p, size_t smem, cudaStream_t st) 
   cfg.attrs = at;
   cfg.numAttrs = 1;
   void* args[] = {const_cast<LatParams*>(&p)};
-  return cudaLaunchKernelExC(&cfg, (const void*)cell_lat_kernel<C>, args);
+  return cudaLaunchKernelExC(&cfg, (const void*)cell_lat_kernel<C, Sh>, args);
 }
 
 // Launches the small-batch kernel with clusters of C CTAs; returns cudaErrorNotSupported
@@ -726,11 +756,23 @@ cudaError_t launch_cell_lat(Handle& h, const CellRun& run, int C, cudaStream_t s
   p.run = run;
   p.trace = h.lat_trace;
   const size_t smem = lat_smem_bytes(h.dims, p.lay);
+  // BASELINE configs 1, 2 (every L) and 3 at their cluster sizes run a kernel specialised
+  // for the shape (FW_LAT_GENERIC=1 forces the generic one)
+  static const bool generic = getenv("FW_LAT_GENERIC") != nullptr;
+  const CellDims& d = h.dims;
+  auto is = [&](int R, int D, int S, int H, int A) {
+    return !generic && d.R == R && d.D == D && d.S == S && d.H == H && d.A == A;
+  };
   switch (C) {
-    case 2: return lat_launch<2>(p, smem, st);
-    case 4: return lat_launch<4>(p, smem, st);
-    case 8: return lat_launch<8>(p, smem, st);
-    case 16: return lat_launch<16>(p, smem, st);
+    case 2:
+      if (is(64, 64, 256, 256, 256)) return lat_launch<2, LatShape<64, 64, 256, 256, 256, 2>>(p, smem, st);
+      return lat_launch<2, LatAnyShape>(p, smem, st);
+    case 4: return lat_launch<4, LatAnyShape>(p, smem, st);
+    case 8: return lat_launch<8, LatAnyShape>(p, smem, st);
+    case 16:
+      if (is(32, 32, 128, 128, 256)) return lat_launch<16, LatShape<32, 32, 128, 128, 256, 16>>(p, smem, st);
+      if (is(128, 128, 256, 256, 256)) return lat_launch<16, LatShape<128, 128, 256, 256, 256, 16>>(p, smem, st);
+      return lat_launch<16, LatAnyShape>(p, smem, st);
     default: return cudaErrorNotSupported;
   }
 }
