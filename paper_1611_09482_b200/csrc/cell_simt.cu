@@ -491,11 +491,23 @@ StagedLayout staged_layout(const CellDims& d, int stages = 3) {
 //   push x_l[t] -> slot; dil partials; [bar] reduce + gate -> z, the pop of layer gg+1 into the
 //   other buffer, prefetch of layer gg+3; [bar] skip|res partials over z (one [D][S+R] weight
 //   matrix); [bar] s += .., x_{l+1} -> the other buffer; [bar]
-template <int BT>
+// Sh: the shape at compile time (kFixed) for BASELINE config 5, so the GEMV loops see
+// constant trip counts; StAnyShape reads it at run time.
+struct StAnyShape {
+  static constexpr bool kFixed = false;
+  static constexpr int R = 0, D = 0, S = 0, H = 0, A = 0;
+};
+template <int R_, int D_, int S_, int H_, int A_>
+struct StShape {
+  static constexpr bool kFixed = true;
+  static constexpr int R = R_, D = D_, S = S_, H = H_, A = A_;
+};
+template <int BT, class Sh = StAnyShape>
 __global__ void __launch_bounds__(kStThreads, 1) cell_staged_kernel(SimtParams p, StagedLayout y) {
   extern __shared__ __align__(1024) float smf[];
   const CellDims d = p.d;
-  const int R = d.R, D = d.D, S = d.S, H = d.H, A = d.A, L = d.L;
+  const int R = Sh::kFixed ? Sh::R : d.R, D = Sh::kFixed ? Sh::D : d.D, S = Sh::kFixed ? Sh::S : d.S,
+            H = Sh::kFixed ? Sh::H : d.H, A = Sh::kFixed ? Sh::A : d.A, L = d.L;
   const int SR = S + R;
   float* xx = smf + y.xx;  // [2][BT][2R]
   float* z = smf + y.z;    // [BT][D]
@@ -684,7 +696,7 @@ bool staged_supported(const CellDims& d) {
          staged_layout<8>(d).stage_bytes >= 4 * 4 * 1024;
 }
 
-template <int BT>
+template <int BT, class Sh = StAnyShape>
 cudaError_t launch_staged(const SimtParams& p, cudaStream_t st) {
   int stages = 3;
   if (const char* ev = getenv("FW_SIMT_STAGES")) stages = max(2, min(kStStagesMax, atoi(ev)));
@@ -692,11 +704,11 @@ cudaError_t launch_staged(const SimtParams& p, cudaStream_t st) {
   if (y.stage_bytes < 4 * 4 * 1024) y = staged_layout<BT>(p.d, 3);
   y.issuers = 4;
   if (const char* ev = getenv("FW_SIMT_ISSUERS")) y.issuers = max(1, min(32, atoi(ev)));
-  cudaError_t e = cudaFuncSetAttribute(cell_staged_kernel<BT>,
+  cudaError_t e = cudaFuncSetAttribute(cell_staged_kernel<BT, Sh>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)y.total);
   if (e != cudaSuccess) return e;
   const int grid = (p.B + BT - 1) / BT;
-  cell_staged_kernel<BT><<<grid, kStThreads, y.total, st>>>(p, y);
+  cell_staged_kernel<BT, Sh><<<grid, kStThreads, y.total, st>>>(p, y);
   return cudaGetLastError();
 }
 
@@ -762,7 +774,11 @@ cudaError_t launch_cell_simt(Handle& h, const CellRun& run, cudaStream_t st,
       case 2: return launch_staged<2>(p, st);
       case 4: return launch_staged<4>(p, st);
       case 6: return launch_staged<6>(p, st);
-      case 7: return launch_staged<7>(p, st);
+      case 7:  // BASELINE config 5 (1,024 streams) at its shape: the specialised kernel
+        if (h.dims.R == 64 && h.dims.D == 64 && h.dims.S == 256 && h.dims.H == 256 &&
+            h.dims.A == 256 && !getenv("FW_LAT_GENERIC"))
+          return launch_staged<7, StShape<64, 64, 256, 256, 256>>(p, st);
+        return launch_staged<7>(p, st);
       default: return launch_staged<8>(p, st);
     }
   }
