@@ -153,10 +153,17 @@ def step_accounting(cell, batch, queue_elem_bytes=4):
     return flops, weight_bytes + queue_bytes + io_bytes, queue_bytes
 
 
-def simt_kernel_name(batch):
-    """The SIMT kernel the library selects (capi launch_cell_simt): one cluster per stream up
-    to 16 streams, else the weight-staged kernel."""
-    return "cell_cluster_kernel" if batch <= 16 else "cell_staged_kernel"
+def simt_kernel_name(cell, batch):
+    """The fp32 kernel the library selects (cell_simt.cu launch_cell_simt): one cluster per
+    stream while the clusters fit the SMs (2 CTAs per stream up to 74 streams), then the
+    warp-MMA kernel for the fp32 configs' shape (R = D = 64, S = H = A = 256), else the
+    weight-staged kernel."""
+    if batch * 2 <= 148:
+        return "cell_lat_kernel"
+    if (cell.residual_channels, cell.dilation_channels, cell.skip_channels, cell.H,
+            cell.classes) == (64, 64, 256, 256, 256) and os.environ.get("FW_SIMT_HMMA") != "0":
+        return "cell_hmma_kernel"
+    return "cell_staged_kernel"
 
 
 def traffic_per_launch(workload, kernel, batch):
@@ -475,13 +482,17 @@ def main():
             roof = {"bound": "hbm", "achieved": bytes_step / k_s / 1e9, "peak": hbm / 1e9,
                     "unit": "GB/s"}
         roof["frac"] = roof["achieved"] / roof["peak"]
-        kfam = "tcgen05" if tc else "simt"
+        kname = "step_kernel" if tc else simt_kernel_name(spec.cell, B)
+        kfam = "tcgen05" if tc else {"cell_lat_kernel": "simt", "cell_hmma_kernel": "hmma",
+                                     "cell_staged_kernel": "simt"}[kname]
         traffic, tsrc = traffic_per_launch(spec.name, kfam, B)
         roof["traffic"] = traffic
         roof["kernel"] = ("step_kernel (persistent: chain + skip sum + heads + selection, one "
                           "cooperative launch per generate call, per-step share)" if tc
-                          else f"{simt_kernel_name(B)} (persistent fp32 SIMT kernel, one launch per "
-                          "generate call, per-step share)")
+                          else f"{kname} (persistent fp32 kernel, one launch per generate call, "
+                          "per-step share" + ("; its products run on the tensor cores as mma.sync "
+                          "with a 3-term fp16 split, reported against the FP32 peak of the fp32 "
+                          "model's FLOPs)" if kname == "cell_hmma_kernel" else ")"))
         roof["algorithmic_per_step"] = {
             "flop": flops, "bytes": bytes_step,
             "queue_bytes": qbytes, "queue_slot_dtype": "fp16" if tc else "fp32",

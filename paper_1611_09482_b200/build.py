@@ -17,7 +17,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfastwavenet.so"
-SOURCES = ["capi.cu", "cell_simt.cu", "cell_lat.cu", "cell_tc.cu", "plain_f64.cu", "prefill.cu"]
+SOURCES = ["capi.cu", "cell_simt.cu", "cell_lat.cu", "cell_hmma.cu", "cell_tc.cu", "plain_f64.cu", "prefill.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

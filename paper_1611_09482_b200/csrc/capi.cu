@@ -75,6 +75,7 @@ void free_cell(Handle& h) {
   if (h.tc) tc_destroy(h);
   prefill_destroy(h);
   lat_destroy(h);
+  hmma_destroy(h);
   if (h.d_pad) cudaFree(h.d_pad);
   if (h.d_pad_lg) cudaFree(h.d_pad_lg);
   h.d_pad = nullptr;

@@ -333,6 +333,18 @@ __device__ __forceinline__ void st_produce(StageRing& rg, const float* W, int K,
   }
 }
 
+// (a0, a1) += (w0, w1) * x on the packed FP32x2 pipe: one FFMA2 with x as a broadcast
+// scalar operand; each lane is the same fused multiply-add as fmaf (bit-identical)
+__device__ __forceinline__ void ffma2(float& a0, float& a1, float w0, float w1, float x) {
+  unsigned long long acc, w;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "f"(a0), "f"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(w) : "f"(w0), "f"(w1));
+  unsigned long long xx;
+  asm("mov.b64 %0, {%1, %1};" : "=l"(xx) : "f"(x));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(w), "l"(xx));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a0), "=f"(a1) : "l"(acc));
+}
+
 // Consumer side, part 1: partial sums of out[b][o] = sum_k W[k][o] in[b][k] (b < BT, o < N,
 // N % 4 == 0, K % 4 == 0, ldin % 4 == 0) into red[g][b][o], one slice per K group g of the
 // thread groups (4 consecutive outputs x BT streams per thread). Returns the group count;
@@ -377,9 +389,17 @@ __device__ __forceinline__ int st_partial_ob(StageRing& rg, const float* in, int
           const float4 x = *reinterpret_cast<const float4*>(in + b * ldin + k0 + k);
           const float xs[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u)
+          for (int u = 0; u < 4; ++u) {
+            if constexpr (OB % 2 == 0) {
+              // output pairs on the packed FP32x2 pipe (FFMA2, the stream's input broadcast):
+              // half the issue slots, the same fused multiply-add per output and order
 #pragma unroll
-            for (int j = 0; j < OB; ++j) acc[j][b] = fmaf(wv[u][j], xs[u], acc[j][b]);
+              for (int j = 0; j < OB; j += 2) ffma2(acc[j][b], acc[j + 1][b], wv[u][j], wv[u][j + 1], xs[u]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < OB; ++j) acc[j][b] = fmaf(wv[u][j], xs[u], acc[j][b]);
+            }
+          }
         }
       }
       if (qq == tid) {
@@ -757,6 +777,13 @@ cudaError_t launch_cell_simt(Handle& h, const CellRun& run, cudaStream_t st,
   // small batches: one cluster of 2..16 CTAs per stream (FW_SIMT_CLUSTER overrides)
   if (const int c = cluster_for(h.dims, B)) {
     const cudaError_t e = launch_cell_lat(h, run, c, st);
+    if (e != cudaErrorNotSupported) return e;
+  }
+  // the fp32 configs' shape (3, 5) past the cluster kernel's batches: the warp-MMA kernel
+  // (cell_hmma.cu; FW_SIMT_HMMA=0 selects the SIMT kernels below)
+  const char* he = getenv("FW_SIMT_HMMA");
+  if (hmma_supported(h.dims) && !(he != nullptr && atoi(he) == 0)) {
+    const cudaError_t e = launch_cell_hmma(h, run, st);
     if (e != cudaErrorNotSupported) return e;
   }
   // mid/large batches: the weight-staged kernel (FW_SIMT_STAGED=0 selects the __ldg kernel)

@@ -42,6 +42,10 @@ struct TcState {
   int64_t* d_qoff = nullptr;  // [L] byte offset of each layer's ring
   int fused = 0, SK = 256, nchain = 0, nskip = 0;
   int split = 0;              // chain tiles split over 2-CTA clusters (small batches)
+  int fold = 0;               // folded chain (chain_fold.cuh): 128-row tiles over 2-CTA clusters
+  uint8_t* wfold = nullptr;   // [L][14 chunks][128 n][64 k] SW128 (chain_fold.cuh)
+  float* fold_b = nullptr;    // [L][2D] dilated bias + W0_l b_res,l-1
+  int fold_has_bias = 0;
   int heads = 0;              // head1 / head2 fused into the skip blocks (needs fused)
   uint8_t* wh1b = nullptr;    // [nsk][S/64][H/nsk rows][128 B] (fused head1)
   uint8_t* wh1 = nullptr;     // [H/128][S/64] chunks of [128][64]
@@ -166,6 +170,7 @@ struct ChainArgs {
   int heads, H;
   int pair_mode;         // tail blocks in 2-CTA clusters exchanging through DSMEM
   int split;             // chain tiles over 2-CTA clusters, one dilated N-half per CTA
+  int fold;              // folded chain: 128-row tiles over 2-CTA clusters (chain_fold.cuh)
   int zpub;              // z stash publications per tile pair per layer (2, or 4 when split)
   uint32_t* sflag;       // [B/128] (cumulative over the launch's steps)
   uint32_t* hflag;       // [B/128]
@@ -585,6 +590,24 @@ uint16_t f16_bits(float f) {
   return u;
 }
 
+uint16_t f16_bits_exact(double v) {
+  __half b = __float2half_rn((float)v);
+  uint16_t u;
+  std::memcpy(&u, &b, 2);
+  return u;
+}
+
+// Rows [0, nrows) of (row, k) -> fp16 bits, K slice [k0, k0+64), as a swizzled image.
+template <typename F>
+void pack_image_bits(uint8_t* dst, int nrows, int k0, F bits) {
+  for (int r = 0; r < nrows; ++r)
+    for (int k = 0; k < 64; ++k) {
+      const size_t off = (size_t)(r >> 3) * 1024 + (r & 7) * 128 + ((((k >> 3) ^ (r & 7))) << 4) + (k & 7) * 2;
+      const uint16_t b = bits(r, k0 + k);
+      std::memcpy(dst + off, &b, 2);
+    }
+}
+
 // Rows [0, nrows) of the (row, k) -> value function, K slice [k0, k0+64), as a swizzled image.
 template <typename F>
 void pack_image(uint8_t* dst, int nrows, int k0, F val) {
@@ -729,6 +752,12 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
     const char* se = getenv("FW_CHAIN_SPLIT");
     tc->split = tc->heads && S == 512 && H == 512 && A == 256 && 2 * tc->nchain + tc->nskip <= sms &&
                 !(se && atoi(se) == 0) && !getenv("FW_NO_CLUSTER");
+    // folded chain (FW_CHAIN_FOLD=1; measured slower): one 128-row tile
+    // per 2-CTA cluster -- the same B/64 chain CTAs as the unsplit kernel, every MMA at M = 128
+    const char* fe = getenv("FW_CHAIN_FOLD");
+    tc->fold = tc->heads && S == 512 && H == 512 && A == 256 && tc->nchain + tc->nskip <= sms &&
+               fe && atoi(fe) != 0 && !getenv("FW_NO_CLUSTER");
+    if (tc->fold) tc->split = 0;
     if (tc->split) tc->nchain *= 2;
     if (tc->heads) {
       std::vector<uint8_t> w1((size_t)nsk * (S / 64) * n1 * 128);
@@ -738,6 +767,55 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
                      [&](int n, int k) { return desc->head1_w[(size_t)(e * n1 + n) * S + k]; });
       if (int rc = upload_bytes(&tc->wh1b, w1)) return rc;
     }
+  }
+  if (tc->fold) {
+    // per layer 14 chunks [128 n][64 k]: W1 / W0 / WF N-halves (tanh rows 64hh.. then sigmoid
+    // rows D + 64hh..) x 2 K-chunks, then Wr_{l-1} x 2 K-chunks; WF_l = W0_l Wr_{l-1} and the
+    // folded bias b_l + W0_l br_{l-1} in fp64 from the bf16-rounded weights
+    const HostCell& c = h.host;
+    const int D2 = 2 * kD;
+    std::vector<uint8_t> img((size_t)L * fold::kLayerBytes, 0);
+    std::vector<float> fb((size_t)L * D2);
+    std::vector<double> wf((size_t)D2 * kD);
+    for (int l = 0; l < L; ++l) {
+      const float* w0 = c.dil_w.data() + ((size_t)l * 2 + 0) * D2 * kR;
+      const float* w1 = c.dil_w.data() + ((size_t)l * 2 + 1) * D2 * kR;
+      const float* wr = l > 0 ? c.res_w.data() + (size_t)(l - 1) * kR * kD : nullptr;
+      const float* br = l > 0 ? c.res_b.data() + (size_t)(l - 1) * kR : nullptr;
+      for (int row = 0; row < D2; ++row) {
+        double b = c.dil_b[(size_t)l * D2 + row];
+        if (l > 0) {
+          for (int j = 0; j < kR; ++j) b += (double)w0[(size_t)row * kR + j] * br[j];
+          for (int k = 0; k < kD; ++k) {
+            double acc = 0;
+            for (int j = 0; j < kR; ++j) acc += (double)w0[(size_t)row * kR + j] * wr[(size_t)j * kD + k];
+            wf[(size_t)row * kD + k] = acc;
+          }
+        }
+        fb[(size_t)l * D2 + row] = (float)b;
+      }
+      uint8_t* base = img.data() + (size_t)l * fold::kLayerBytes;
+      auto row_of = [&](int hh, int n) { return n < 64 ? 64 * hh + n : kD + 64 * hh + (n - 64); };
+      for (int hh = 0; hh < 2; ++hh)
+        for (int kc = 0; kc < 2; ++kc) {
+          pack_image(base + (size_t)(0 + 2 * hh + kc) * kChunk, 128, kc * 64,
+                     [&](int n, int k) { return w1[(size_t)row_of(hh, n) * kR + k]; });
+          pack_image(base + (size_t)(4 + 2 * hh + kc) * kChunk, 128, kc * 64,
+                     [&](int n, int k) { return w0[(size_t)row_of(hh, n) * kR + k]; });
+          if (l > 0)
+            pack_image_bits(base + (size_t)(8 + 2 * hh + kc) * kChunk, 128, kc * 64, [&](int n, int k) {
+              return f16_bits_exact(wf[(size_t)row_of(hh, n) * kD + k]);
+            });
+        }
+      if (l > 0)
+        for (int kc = 0; kc < 2; ++kc)
+          pack_image(base + (size_t)(12 + kc) * kChunk, 128, kc * 64,
+                     [&](int n, int k) { return wr[(size_t)n * kD + k]; });
+    }
+    if (int rc = upload_bytes(&tc->wfold, img)) return rc;
+    for (float v : fb) tc->fold_has_bias |= (v != 0.f);
+    if (int rc = dev_alloc(&tc->fold_b, sizeof(float) * fb.size())) return rc;
+    cudaMemcpy(tc->fold_b, fb.data(), sizeof(float) * fb.size(), cudaMemcpyHostToDevice);
   }
   {
     std::vector<uint8_t> img((size_t)(H / 128) * (S / 64) * kTile);
@@ -766,6 +844,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
   if (int rc = dev_alloc(&tc->himg, (size_t)tc->ntile * (H / 64) * kTile)) return rc;
   if (int rc = dev_alloc(&tc->cls, sizeof(int32_t) * h.batch)) return rc;
   cudaError_t e = set_smem(step_kernel, kChainSmem);
+  if (e == cudaSuccess) e = set_smem(step_kernel_fold, kChainSmem);
   if (e == cudaSuccess) e = set_smem(gemm_kernel<128, 0>, gemm_smem<128>());
   if (e == cudaSuccess) e = set_smem(gemm_kernel<256, 1>, gemm_smem<256>());
   if (e != cudaSuccess) {
@@ -778,7 +857,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
 void tc_destroy(Handle& h) {
   TcState* tc = h.tc;
   if (!tc) return;
-  void* ptrs[] = {tc->wchain, tc->wskip, tc->wskip2, tc->zflag, tc->d_qoff, tc->wh1b, tc->wh1, tc->wh2, tc->skip_bsum,
+  void* ptrs[] = {tc->wfold, tc->fold_b, tc->wchain, tc->wskip, tc->wskip2, tc->zflag, tc->d_qoff, tc->wh1b, tc->wh1, tc->wh2, tc->skip_bsum,
                   tc->zimg, tc->simg, tc->himg, tc->cls};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -797,13 +876,14 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.B = B;
   ca.L = L;
   ca.queue = reinterpret_cast<uint8_t*>(h.d_queue);
-  ca.w = tc->wchain;
+  ca.fold = tc->fold;
+  ca.w = tc->fold ? tc->wfold : tc->wchain;
   ca.embed = h.w.embed;
-  ca.dil_b = h.w.dil_b;
+  ca.dil_b = tc->fold ? tc->fold_b : h.w.dil_b;
   ca.res_b = h.w.res_b;
   ca.cls = tc->cls;
   ca.zimg = tc->zimg;
-  ca.has_dil_bias = tc->has_dil_bias;
+  ca.has_dil_bias = tc->fold ? tc->fold_has_bias : tc->has_dil_bias;
   ca.has_res_bias = tc->has_res_bias;
   ca.trace = tc->trace;
   const int npairs_all = B / 128;
@@ -910,8 +990,9 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
         at[1].val.clusterDim.y = 1;
         at[1].val.clusterDim.z = 1;
         cfg.attrs = at;
-        cfg.numAttrs = ca.pair_mode ? 2 : 1;  // the cluster dimension only for the pair tail
-        e = cudaLaunchKernelExC(&cfg, (const void*)step_kernel, kargs);
+        // the cluster dimension for the pair tail (and the split / folded chain, which need it)
+        cfg.numAttrs = (ca.pair_mode || ca.fold) ? 2 : 1;
+        e = cudaLaunchKernelExC(&cfg, ca.fold ? (const void*)step_kernel_fold : (const void*)step_kernel, kargs);
       }
       if (e != cudaSuccess) return e;
     }

@@ -671,6 +671,9 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
 
+#include "chain_fold.cuh"
+static_assert(fold::kSmem <= kChainSmem, "folded chain shared memory");
+
 // One launch per step: blocks [0, nchain) run the chain of one 64-stream tile each, blocks
 // [nchain, nchain + nskip) the skip role (when fused; launched cooperatively so that all
 // blocks are co-resident -- the skip blocks wait on the chain blocks).
@@ -1367,3 +1370,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel(ChainArgs a) {
   if (split) cluster_sync();  // no DSMEM copy into a CTA that has exited
   if (warp == 1) tmem_dealloc(tmem, 512);
 }
+
+// The folded chain (FW_CHAIN_FOLD=1, chain_fold.cuh) as its own kernel, so the default step
+// kernel's code and register allocation are those the race checks ran on.
+__global__ void __launch_bounds__(kChainThreads, 1) step_kernel_fold(ChainArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  if ((int)blockIdx.x >= a.nchain) {
+    if (a.pair_mode && cluster_size() == 2)
+      tail_pair_role(a, smem, (int)blockIdx.x - a.nchain);
+    else
+      skip_role(a, smem, (int)blockIdx.x - a.nchain);
+    return;
+  }
+  chain_fold_role(a, smem);
+}
+

@@ -94,6 +94,8 @@ struct TcState;
 struct LatPlan;
 // full-sequence prefill state (see prefill.cu).
 struct PrefillState;
+// warp-MMA kernel's fragment images (see cell_hmma.cu).
+struct HmmaPlan;
 
 struct Handle;
 
@@ -103,6 +105,9 @@ cudaError_t launch_cell_simt(Handle& h, const CellRun& run, cudaStream_t st,
 cudaError_t launch_cell_lat(Handle& h, const CellRun& run, int C, cudaStream_t st);
 bool lat_supported(const CellDims& d, int C);
 void lat_destroy(Handle& h);
+cudaError_t launch_cell_hmma(Handle& h, const CellRun& run, cudaStream_t st);
+bool hmma_supported(const CellDims& d);
+void hmma_destroy(Handle& h);
 cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64_t* launches);
 bool tc_supported(const CellDims& d, int batch, std::string* why);
 int tc_create(Handle& h, const fw_cell_desc* desc);
@@ -176,6 +181,7 @@ struct Handle {
   TcState* tc = nullptr;
   PrefillState* prefill = nullptr;
   LatPlan* lat = nullptr;
+  HmmaPlan* hmma = nullptr;
   long long* lat_trace = nullptr;  // fw_debug_trace on a SIMT handle: small-batch kernel stamps
   HostCell host;
 

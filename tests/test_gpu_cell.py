@@ -329,6 +329,8 @@ def test_staged_simt_kernel_matches_oracle_and_ldg_kernel(cuda, monkeypatch, bt)
     GEMVs span several stages (R = 128, S = H = 512) and non-zero biases, and continues a
     free run with the __ldg kernel's classes."""
     monkeypatch.setenv("FW_SIMT_BT", bt)
+    monkeypatch.setenv("FW_SIMT_CLUSTER", "0")  # (these batches would take the cluster kernel,
+    monkeypatch.setenv("FW_SIMT_HMMA", "0")     # and the R = D = 64 shape the warp-MMA one)
     for cfg, B in ((CellConfig(2, 3, 64, 64, 256, bias="fan_in", init_seed=4), 37),
                    (CellConfig(1, 4, 128, 128, 512, bias="fan_in", init_seed=6), 19)):
         m = build_cell_model(cfg)
@@ -392,3 +394,42 @@ def test_small_batch_kernel_streamed_weights(cuda, monkeypatch, cluster):
         ref = o.forward_full(cls[:, b])
         assert np.max(np.abs(lg[:, b] - ref)) <= 1e-4, (cluster, b)
         assert np.array_equal(out[:, b], np.argmax(lg[:, b], axis=1))
+
+
+@pytest.mark.parametrize("B,nt", [(37, "1"), (130, "1"), (37, "2")])
+def test_warp_mma_kernel_matches_oracle(cuda, monkeypatch, B, nt):
+    """The fp32 configs' warp-MMA kernel (cell_hmma.cu: 3-term fp16 split products on
+    mma.sync, skip of layer l - 1 interleaved with the dilated GEMM of layer l, the running
+    sums in fp32): teacher-forced logits within 1e-4 of the oracle with non-zero biases, a
+    partly filled last CTA (8 or 16 streams per CTA), and free runs (Gumbel, inverse CDF)
+    choice by choice on the kernel's own history."""
+    monkeypatch.setenv("FW_SIMT_CLUSTER", "0")
+    monkeypatch.setenv("FW_HMMA_NT", nt)
+    cfg = CellConfig(2, 4, 64, 64, 256, bias="fan_in", init_seed=9)
+    m = build_cell_model(cfg)
+    n = 40
+    cls = np.random.default_rng(B).integers(0, 256, (n, B))
+    out, lg = run(CellGenerator(m, B, kernel="simt"), cls, n, Sampler(0), n)
+    o = oc.CellOracle(m)
+    for b in (0, 7, 8, B // 2, B - 1):
+        ref = o.forward_full(cls[:, b])
+        assert np.max(np.abs(lg[:, b] - ref)) <= 1e-4, (B, b, np.max(np.abs(lg[:, b] - ref)))
+    primer = cls[:3]
+    for mode in (configs.SAMPLE_GUMBEL, configs.SAMPLE_INVCDF):
+        tie = 2e-4 if mode == configs.SAMPLE_GUMBEL else 1e-5
+        got, _ = run(CellGenerator(m, B, kernel="simt"), primer, 60, Sampler(mode, 13), 0)
+        check_streams(o, primer, got, None, [0, 9, B - 1], mode, 13, 1e-4, tie)
+
+
+def test_warp_mma_kernel_agrees_with_staged_kernel(cuda, monkeypatch):
+    """cfg5's shape on 300 streams: the warp-MMA kernel and the weight-staged SIMT kernel
+    (exact fp32 FMAs) give the same teacher-forced logits to 1e-4 over 100 steps."""
+    spec = configs.cfg5()
+    m = build_cell_model(spec.cell)
+    B, n = 300, 100
+    cls = np.random.default_rng(5).integers(0, 256, (n, B))
+    _, lg_m = run(CellGenerator(m, B, kernel="simt"), cls, n, Sampler(0), n)
+    monkeypatch.setenv("FW_SIMT_HMMA", "0")
+    _, lg_s = run(CellGenerator(m, B, kernel="simt"), cls, n, Sampler(0), n)
+    assert np.max(np.abs(lg_m - lg_s)) <= 1e-4
+

@@ -14,7 +14,8 @@ invariants, pkg/tests/test_acceptance.py:139-155).
   folded pair tail, head2 accumulating onto bias + noise), every choice of 8 streams
   margin-checked against the oracle on the GPU's own history.
 * cfg5 (d_max 2,048): BASELINE's own check -- 1,024 streams teacher-forced on the seeded
-  random walk, logits compared on 2,100 steps (past the 2,048 wrap).
+  random walk, logits compared on 2,100 steps (past the 2,048 wrap), on the warp-MMA kernel
+  and on the weight-staged SIMT kernel.
 * cfg3 (d_max 512): 600 Gumbel steps, 64 streams; cfg2: the full 1,000 steps at every L.
 
 Tolerances are the north-star's: logits 1e-4 (fp32 configs) / 2e-2 (bf16 config) max-abs;
@@ -98,9 +99,12 @@ def test_cfg4_tcgen05_gumbel_free_run_folded_tail(cuda, cfg4_model):
     assert len(np.unique(out[:, CFG4_STREAMS])) > 20
 
 
-def test_cfg5_baseline_check_2100_steps(cuda):
+@pytest.mark.parametrize("hmma", ["1", "0"])
+def test_cfg5_baseline_check_2100_steps(cuda, monkeypatch, hmma):
     """BASELINE cfg5: 1,024 streams teacher-forced on the random walk, logits compared with
-    the CPU path on the first steps -- here 2,100 (> d_max = 2,048)."""
+    the CPU path on the first steps -- here 2,100 (> d_max = 2,048); on the warp-MMA kernel
+    (the default) and on the weight-staged SIMT kernel."""
+    monkeypatch.setenv("FW_SIMT_HMMA", hmma)
     spec = configs.cfg5()
     m = build_cell_model(spec.cell)
     n = 2100
@@ -203,14 +207,17 @@ def test_tcgen05_repeated_runs_are_bit_identical(cuda, cfg4_model, monkeypatch, 
         del lg
 
 
-@pytest.mark.parametrize("config,batch,cluster", [("cfg1", 1, ""), ("cfg2_L8", 2, "16"),
-                                                  ("cfg3", 64, ""), ("cfg5", 1024, "")])
-def test_simt_repeated_runs_are_bit_identical(cuda, monkeypatch, config, batch, cluster):
+@pytest.mark.parametrize("config,batch,cluster,hmma", [("cfg1", 1, "", "1"), ("cfg2_L8", 2, "16", "1"),
+                                                       ("cfg3", 64, "", "1"), ("cfg5", 1024, "", "1"),
+                                                       ("cfg5", 1024, "", "0")])
+def test_simt_repeated_runs_are_bit_identical(cuda, monkeypatch, config, batch, cluster, hmma):
     """Race detector for the fp32 kernels (the small-batch cluster kernel's st.async
-    exchanges and weight ring, the staged kernel's producer/consumer ring): three identical
-    teacher-forced runs, past the largest ring wrap where affordable, agree bit for bit."""
+    exchanges and weight ring, the warp-MMA and staged kernels' producer/consumer rings):
+    three identical teacher-forced runs, past the largest ring wrap where affordable, agree
+    bit for bit."""
     if cluster:
         monkeypatch.setenv("FW_SIMT_CLUSTER", cluster)
+    monkeypatch.setenv("FW_SIMT_HMMA", hmma)
     spec = configs.by_name(config)
     m = build_cell_model(spec.cell)
     n = 300 if config == "cfg5" else 600
