@@ -428,11 +428,8 @@ __global__ void __launch_bounds__(kHmThreads, 1) cell_hmma_kernel(HmmaParams p, 
         float dacc[NT][3][4] = {};
         float sacc[2][NT][3][4] = {};
 #pragma unroll
-        long long wsum = 0;
         for (int q = 0; q < KT1 / 2; ++q) {
-          const long long w0 = tr ? clock64() : 0;
           ptx::mbar_wait(&rg.full[rg.slot], rg.ph);
-          if (tr) wsum += clock64() - w0;
           const uint8_t* st = rg.buf + (size_t)rg.slot * kHmStage + lane16;
 #pragma unroll
           for (int kk = 0; kk < 2; ++kk) {
@@ -465,10 +462,7 @@ __global__ void __launch_bounds__(kHmThreads, 1) cell_hmma_kernel(HmmaParams p, 
           if (lane == 0) ptx::mbar_arrive(&rg.empty[rg.slot]);
           rg.advance();
         }
-        if (tr) {
-          tr[1] = clock64();
-          tr[7] = wsum;  // cycles thread 0 waited for phase A's weight stages
-        }
+        if (tr) tr[1] = clock64();
         // gate: a thread holds tanh and sigmoid inputs of channel 8 warp + g for streams
         // 8 nt + 2 t4 + {0, 1}
         const int ch = 8 * warp + g;

@@ -19,13 +19,13 @@ x = torch.full((1, spec.batch), 128, dtype=torch.int32, device="cuda")
 gen.generate(x, 3, Sampler(0))
 torch.cuda.synchronize()
 t = tr.view(L + 2, 8).cpu().numpy().astype(np.int64)
-print("layer period  gemmA   epiA   pops   bar1 phaseB   bar2  waitA")
+print("layer period  gemmA   epiA   pops   bar1 phaseB   bar2   next")
 per = []
 for l in range(L):
-    d = [t[l, k] - t[l, k - 1] for k in range(1, 7)] + [t[l, 7]]
+    d = [t[l, k] - t[l, k - 1] for k in range(1, 7)] + [(t[l + 1, 0] if l + 1 < L else t[l, 6]) - t[l, 6]]
     pd = t[l, 0] - t[l - 1, 0] if l else 0
     if l > 1:
         per.append(pd)
     if l < 12 or l == L - 1:
         print(f"{l:5d} {pd:6d} " + " ".join(f"{v:6d}" for v in d))
-print("median period", np.median(per), "median phases", np.median(np.diff(t[2:L, :7], axis=1), axis=0).tolist(), 'waitA', np.median(t[2:L, 7]))
+print("median period", np.median(per), "median phases", np.median(np.diff(t[2:L, :7], axis=1), axis=0).tolist())
