@@ -15,8 +15,8 @@ the same objects to the GPU path:
   identical config gives bit-identical float64 weights to the reference.
   ``tests/golden/plain_*.npz`` pins this against weights the reference built.
 
-The model text format (``model.py:195-306``) is out of scope for this round
-(SURVEY.md section 8(f) rank 3).
+The model text format (``model.py:195-306``) is read and written byte-compatibly by
+``model_io.py``.
 """
 
 from __future__ import annotations
