@@ -46,6 +46,8 @@ struct TcState {
   uint8_t* wfold = nullptr;   // [L][14 chunks][128 n][64 k] SW128 (chain_fold.cuh)
   float* fold_b = nullptr;    // [L][2D] dilated bias + W0_l b_res,l-1
   int fold_has_bias = 0;
+  int cg2 = 0;                // 2-SM chain (chain_2sm.cuh): tile pairs as 2-CTA clusters
+  uint8_t* w2sm = nullptr;    // [L][2 CTAs][5 stages][64 n][128 k] SW128
   int heads = 0;              // head1 / head2 fused into the skip blocks (needs fused)
   uint8_t* wh1b = nullptr;    // [nsk][S/64][H/nsk rows][128 B] (fused head1)
   uint8_t* wh1 = nullptr;     // [H/128][S/64] chunks of [128][64]
@@ -758,6 +760,12 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
     tc->fold = tc->heads && S == 512 && H == 512 && A == 256 && tc->nchain + tc->nskip <= sms &&
                fe && atoi(fe) != 0 && !getenv("FW_NO_CLUSTER");
     if (tc->fold) tc->split = 0;
+    // 2-SM chain (FW_CHAIN_2SM=1): the unsplit grid, tile pairs as clusters issuing
+    // cta_group::2 MMAs (chain_2sm.cuh)
+    const char* ce = getenv("FW_CHAIN_2SM");
+    tc->cg2 = !tc->fold && tc->heads && S == 512 && H == 512 && A == 256 &&
+              tc->nchain + tc->nskip <= sms && ce && atoi(ce) != 0 && !getenv("FW_NO_CLUSTER");
+    if (tc->cg2) tc->split = 0;
     if (tc->split) tc->nchain *= 2;
     if (tc->heads) {
       std::vector<uint8_t> w1((size_t)nsk * (S / 64) * n1 * 128);
@@ -767,6 +775,33 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
                      [&](int n, int k) { return desc->head1_w[(size_t)(e * n1 + n) * S + k]; });
       if (int rc = upload_bytes(&tc->wh1b, w1)) return rc;
     }
+  }
+  if (tc->cg2) {
+    // per layer, per CTA r of a pair: 5 stages [64 n][128 k] (2 SW128 K-chunks each) in MMA
+    // order: x_{t-d} taps of N-halves 0, 1, x_t taps of N-halves 0, 1, residual. Dilated
+    // N-half h, CTA r: rows 0..31 tanh of channels 64h + 32r + j, rows 32..63 their sigmoid;
+    // residual, CTA r: output channels 64r .. 64r + 63
+    const HostCell& c = h.host;
+    std::vector<uint8_t> img((size_t)L * c2::kLayerBytes, 0);
+    for (int l = 0; l < L; ++l)
+      for (int r = 0; r < 2; ++r) {
+        uint8_t* base = img.data() + (size_t)l * c2::kLayerBytes + (size_t)r * c2::kLayerStages * c2::kHalfW;
+        const float* w0 = c.dil_w.data() + ((size_t)l * 2 + 0) * 2 * kD * kR;
+        const float* w1 = c.dil_w.data() + ((size_t)l * 2 + 1) * 2 * kD * kR;
+        auto row_of = [&](int hh, int n) { return n < 32 ? 64 * hh + 32 * r + n : kD + 64 * hh + 32 * r + (n - 32); };
+        for (int s = 0; s < 4; ++s) {
+          const int hh = s & 1;
+          const float* wt = s < 2 ? w1 : w0;
+          for (int kc = 0; kc < 2; ++kc)
+            pack_image(base + (size_t)s * c2::kHalfW + (size_t)kc * 8192, 64, kc * 64,
+                       [&](int n, int k) { return wt[(size_t)row_of(hh, n) * kR + k]; });
+        }
+        const float* wr = c.res_w.data() + (size_t)l * kR * kD;
+        for (int kc = 0; kc < 2; ++kc)
+          pack_image(base + (size_t)4 * c2::kHalfW + (size_t)kc * 8192, 64, kc * 64,
+                     [&](int n, int k) { return wr[(size_t)(64 * r + n) * kD + k]; });
+      }
+    if (int rc = upload_bytes(&tc->w2sm, img)) return rc;
   }
   if (tc->fold) {
     // per layer 14 chunks [128 n][64 k]: W1 / W0 / WF N-halves (tanh rows 64hh.. then sigmoid
@@ -845,6 +880,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
   if (int rc = dev_alloc(&tc->cls, sizeof(int32_t) * h.batch)) return rc;
   cudaError_t e = set_smem(step_kernel, kChainSmem);
   if (e == cudaSuccess) e = set_smem(step_kernel_fold, kChainSmem);
+  if (e == cudaSuccess) e = set_smem(step_kernel_2sm, kChainSmem);
   if (e == cudaSuccess) e = set_smem(gemm_kernel<128, 0>, gemm_smem<128>());
   if (e == cudaSuccess) e = set_smem(gemm_kernel<256, 1>, gemm_smem<256>());
   if (e != cudaSuccess) {
@@ -857,7 +893,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
 void tc_destroy(Handle& h) {
   TcState* tc = h.tc;
   if (!tc) return;
-  void* ptrs[] = {tc->wfold, tc->fold_b, tc->wchain, tc->wskip, tc->wskip2, tc->zflag, tc->d_qoff, tc->wh1b, tc->wh1, tc->wh2, tc->skip_bsum,
+  void* ptrs[] = {tc->w2sm, tc->wfold, tc->fold_b, tc->wchain, tc->wskip, tc->wskip2, tc->zflag, tc->d_qoff, tc->wh1b, tc->wh1, tc->wh2, tc->skip_bsum,
                   tc->zimg, tc->simg, tc->himg, tc->cls};
   for (void* p : ptrs)
     if (p) cudaFree(p);
@@ -877,7 +913,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.L = L;
   ca.queue = reinterpret_cast<uint8_t*>(h.d_queue);
   ca.fold = tc->fold;
-  ca.w = tc->fold ? tc->wfold : tc->wchain;
+  ca.w = tc->fold ? tc->wfold : tc->cg2 ? tc->w2sm : tc->wchain;
   ca.embed = h.w.embed;
   ca.dil_b = tc->fold ? tc->fold_b : h.w.dil_b;
   ca.res_b = h.w.res_b;
@@ -991,8 +1027,10 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
         at[1].val.clusterDim.z = 1;
         cfg.attrs = at;
         // the cluster dimension for the pair tail (and the split / folded chain, which need it)
-        cfg.numAttrs = (ca.pair_mode || ca.fold) ? 2 : 1;
-        e = cudaLaunchKernelExC(&cfg, ca.fold ? (const void*)step_kernel_fold : (const void*)step_kernel, kargs);
+        cfg.numAttrs = (ca.pair_mode || ca.fold || tc->cg2) ? 2 : 1;
+        e = cudaLaunchKernelExC(&cfg, ca.fold ? (const void*)step_kernel_fold
+                                      : tc->cg2 ? (const void*)step_kernel_2sm
+                                                : (const void*)step_kernel, kargs);
       }
       if (e != cudaSuccess) return e;
     }

@@ -673,6 +673,8 @@ __device__ __forceinline__ void tail_pair_role(const ChainArgs& a, uint8_t* smem
 
 #include "chain_fold.cuh"
 static_assert(fold::kSmem <= kChainSmem, "folded chain shared memory");
+#include "chain_2sm.cuh"
+static_assert(c2::kSmem <= kChainSmem, "2-SM chain shared memory");
 
 // One launch per step: blocks [0, nchain) run the chain of one 64-stream tile each, blocks
 // [nchain, nchain + nskip) the skip role (when fused; launched cooperatively so that all
@@ -1384,5 +1386,19 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel_fold(ChainArgs a
     return;
   }
   chain_fold_role(a, smem);
+}
+
+// The 2-SM chain (chain_2sm.cuh) with the same tail roles.
+__global__ void __launch_bounds__(kChainThreads, 1) step_kernel_2sm(ChainArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  if ((int)blockIdx.x >= a.nchain) {
+    if (a.pair_mode && cluster_size() == 2)
+      tail_pair_role(a, smem, (int)blockIdx.x - a.nchain);
+    else
+      skip_role(a, smem, (int)blockIdx.x - a.nchain);
+    return;
+  }
+  chain_2sm_role(a, smem);
 }
 

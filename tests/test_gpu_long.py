@@ -234,3 +234,34 @@ def test_simt_repeated_runs_are_bit_identical(cuda, monkeypatch, config, batch, 
             continue
         bad = torch.nonzero((lg - ref).abs().amax(dim=2) > 0)
         assert bad.shape[0] == 0, bad[:8].tolist()
+
+
+@pytest.mark.parametrize("variant,env", [("2sm", "FW_CHAIN_2SM"), ("fold", "FW_CHAIN_FOLD")])
+def test_opt_in_tcgen05_chains(cuda, cfg4_model, monkeypatch, variant, env):
+    """The opt-in chain variants on all 4,096 cfg4 streams, 120 teacher-forced steps: the
+    2-SM chain (cta_group::2 MMAs, chain_2sm.cuh) does the same arithmetic as the default
+    chain, so its logits are bit-identical; the folded chain (chain_fold.cuh) rounds the
+    folded weights once more and stays within the bf16 tolerance of the default and the
+    oracle. Both twice, bit for bit (race check)."""
+    B, n = configs.cfg4().batch, 120
+    cls = np.random.default_rng(11).integers(0, 256, (n, B)).astype(np.int32)
+    ref = CellGenerator(cfg4_model, B, kernel="tcgen05")
+    _, lg_ref, lg_ref_all = _run(ref, cls, n, Sampler(0), n, CFG4_STREAMS)
+    ref.close()
+    monkeypatch.setenv(env, "1")
+    runs = []
+    for _ in range(2):
+        gen = CellGenerator(cfg4_model, B, kernel="tcgen05")
+        out, lg, lg_all = _run(gen, cls, n, Sampler(0), n, CFG4_STREAMS)
+        gen.close()
+        runs.append(lg_all)
+    assert torch.equal(runs[0], runs[1])
+    if variant == "2sm":
+        assert torch.equal(runs[0], lg_ref_all)
+    else:
+        dev = max(float((runs[0][t:t + 40] - lg_ref_all[t:t + 40]).abs().max()) for t in range(0, n, 40))
+        assert dev <= 2e-2, dev
+        report = []
+        check_streams(oc.CellOracle(cfg4_model, exact=False), cls[:, CFG4_STREAMS], out[:, CFG4_STREAMS],
+                      lg, range(len(CFG4_STREAMS)), 0, 0, 2e-2, 4e-2, report=report, gids=CFG4_STREAMS)
+

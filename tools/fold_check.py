@@ -1,7 +1,7 @@
-"""Folded chain vs the round-2 chain on the cfg4 shape: teacher-forced logits of every stream,
-a few streams against the fp64 oracle, and repeated-run determinism.
+"""An opt-in tcgen05 chain variant vs the default chain on the cfg4 shape: teacher-forced
+logits of every stream, a few streams against the fp64 oracle, and repeated-run determinism.
 
-python tools/fold_check.py BATCH STEPS [REPEATS]
+python tools/fold_check.py BATCH STEPS [REPEATS] [ENV]    (ENV: FW_CHAIN_FOLD | FW_CHAIN_2SM)
 """
 import os
 import sys
@@ -20,13 +20,14 @@ from paper_1611_09482_b200 import CellGenerator, Sampler, build_cell_model, conf
 B = int(sys.argv[1])
 n = int(sys.argv[2])
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
+ENV = sys.argv[4] if len(sys.argv) > 4 else "FW_CHAIN_FOLD"
 m = build_cell_model(configs.cfg4().cell)
 cls = torch.as_tensor(np.random.default_rng(B + 3).integers(0, 256, (n, B)), dtype=torch.int32,
                       device="cuda")
 
 
 def run(fold):
-    os.environ["FW_CHAIN_FOLD"] = fold
+    os.environ[ENV] = fold
     gen = CellGenerator(m, B, kernel="tcgen05")
     t = time.time()
     out, lg = gen.generate(cls, n, Sampler(0), n_logit_steps=n)
