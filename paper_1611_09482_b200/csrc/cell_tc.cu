@@ -765,6 +765,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
     const char* ce = getenv("FW_CHAIN_2SM");
     tc->cg2 = !tc->fold && tc->heads && S == 512 && H == 512 && A == 256 &&
               tc->nchain + tc->nskip <= sms && ce && atoi(ce) != 0 && !getenv("FW_NO_CLUSTER");
+    if (tc->cg2 && atoi(ce) == 2) tc->cg2 = 2;  // the folded 2-SM chain
     if (tc->cg2) tc->split = 0;
     if (tc->split) tc->nchain *= 2;
     if (tc->heads) {
@@ -777,17 +778,38 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
     }
   }
   if (tc->cg2) {
-    // per layer, per CTA r of a pair: 5 stages [64 n][128 k] (2 SW128 K-chunks each) in MMA
-    // order: x_{t-d} taps of N-halves 0, 1, x_t taps of N-halves 0, 1, residual. Dilated
-    // N-half h, CTA r: rows 0..31 tanh of channels 64h + 32r + j, rows 32..63 their sigmoid;
-    // residual, CTA r: output channels 64r .. 64r + 63
+    // per layer, per CTA r of a pair, 16 KB halves [64 n][128 k] (2 SW128 K-chunks each) in
+    // MMA order: x_{t-d} taps of N-halves 0, 1, x_t taps of N-halves 0, 1, (folded: WF_l =
+    // W0_l Wr_{l-1} of N-halves 0, 1,) residual. Dilated N-half h, CTA r: rows 0..31 tanh of
+    // channels 64h + 32r + j, rows 32..63 their sigmoid; residual, CTA r: output channels
+    // 64r .. 64r + 63
     const HostCell& c = h.host;
-    std::vector<uint8_t> img((size_t)L * c2::kLayerBytes, 0);
-    for (int l = 0; l < L; ++l)
+    const bool f2 = tc->cg2 == 2;
+    const int nh = f2 ? c2::kLayerStagesF : c2::kLayerStages;
+    const size_t lbytes = (size_t)2 * nh * c2::kHalfW;
+    std::vector<uint8_t> img((size_t)L * lbytes, 0);
+    std::vector<float> fb((size_t)L * 2 * kD);
+    std::vector<double> wf((size_t)2 * kD * kD);
+    for (int l = 0; l < L; ++l) {
+      const float* w0 = c.dil_w.data() + ((size_t)l * 2 + 0) * 2 * kD * kR;
+      const float* w1 = c.dil_w.data() + ((size_t)l * 2 + 1) * 2 * kD * kR;
+      const float* wr = c.res_w.data() + (size_t)l * kR * kD;
+      const float* wrp = l > 0 ? c.res_w.data() + (size_t)(l - 1) * kR * kD : nullptr;
+      for (int row = 0; row < 2 * kD; ++row) {
+        double b = c.dil_b[(size_t)l * 2 * kD + row];
+        if (l > 0) {
+          for (int j = 0; j < kR; ++j) b += (double)w0[(size_t)row * kR + j] * c.res_b[(size_t)(l - 1) * kR + j];
+          if (f2)
+            for (int k = 0; k < kD; ++k) {
+              double acc = 0;
+              for (int j = 0; j < kR; ++j) acc += (double)w0[(size_t)row * kR + j] * wrp[(size_t)j * kD + k];
+              wf[(size_t)row * kD + k] = acc;
+            }
+        }
+        fb[(size_t)l * 2 * kD + row] = (float)b;
+      }
       for (int r = 0; r < 2; ++r) {
-        uint8_t* base = img.data() + (size_t)l * c2::kLayerBytes + (size_t)r * c2::kLayerStages * c2::kHalfW;
-        const float* w0 = c.dil_w.data() + ((size_t)l * 2 + 0) * 2 * kD * kR;
-        const float* w1 = c.dil_w.data() + ((size_t)l * 2 + 1) * 2 * kD * kR;
+        uint8_t* base = img.data() + (size_t)l * lbytes + (size_t)r * nh * c2::kHalfW;
         auto row_of = [&](int hh, int n) { return n < 32 ? 64 * hh + 32 * r + n : kD + 64 * hh + 32 * r + (n - 32); };
         for (int s = 0; s < 4; ++s) {
           const int hh = s & 1;
@@ -796,12 +818,28 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
             pack_image(base + (size_t)s * c2::kHalfW + (size_t)kc * 8192, 64, kc * 64,
                        [&](int n, int k) { return wt[(size_t)row_of(hh, n) * kR + k]; });
         }
-        const float* wr = c.res_w.data() + (size_t)l * kR * kD;
-        for (int kc = 0; kc < 2; ++kc)
-          pack_image(base + (size_t)4 * c2::kHalfW + (size_t)kc * 8192, 64, kc * 64,
-                     [&](int n, int k) { return wr[(size_t)(64 * r + n) * kD + k]; });
+        int sres = 4;
+        if (f2) {
+          for (int hh = 0; hh < 2 && l > 0; ++hh)
+            for (int kc = 0; kc < 2; ++kc)
+              pack_image_bits(base + (size_t)(4 + hh) * c2::kHalfW + (size_t)kc * 8192, 64, kc * 64,
+                              [&](int n, int k) { return f16_bits_exact(wf[(size_t)row_of(hh, n) * kD + k]); });
+          sres = 6;
+        }
+        // residual of this layer (unfolded) / of layer l - 1 (folded: x_l = x_{l-1} + Wr_{l-1} z)
+        const float* wres = f2 ? wrp : wr;
+        if (wres)
+          for (int kc = 0; kc < 2; ++kc)
+            pack_image(base + (size_t)sres * c2::kHalfW + (size_t)kc * 8192, 64, kc * 64,
+                       [&](int n, int k) { return wres[(size_t)(64 * r + n) * kD + k]; });
       }
+    }
     if (int rc = upload_bytes(&tc->w2sm, img)) return rc;
+    if (f2) {
+      for (float v : fb) tc->fold_has_bias |= (v != 0.f);
+      if (int rc = dev_alloc(&tc->fold_b, sizeof(float) * fb.size())) return rc;
+      cudaMemcpy(tc->fold_b, fb.data(), sizeof(float) * fb.size(), cudaMemcpyHostToDevice);
+    }
   }
   if (tc->fold) {
     // per layer 14 chunks [128 n][64 k]: W1 / W0 / WF N-halves (tanh rows 64hh.. then sigmoid
@@ -881,6 +919,7 @@ int tc_create(Handle& h, const fw_cell_desc* desc) {
   cudaError_t e = set_smem(step_kernel, kChainSmem);
   if (e == cudaSuccess) e = set_smem(step_kernel_fold, kChainSmem);
   if (e == cudaSuccess) e = set_smem(step_kernel_2sm, kChainSmem);
+  if (e == cudaSuccess) e = set_smem(step_kernel_2sf, kChainSmem);
   if (e == cudaSuccess) e = set_smem(gemm_kernel<128, 0>, gemm_smem<128>());
   if (e == cudaSuccess) e = set_smem(gemm_kernel<256, 1>, gemm_smem<256>());
   if (e != cudaSuccess) {
@@ -915,11 +954,11 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
   ca.fold = tc->fold;
   ca.w = tc->fold ? tc->wfold : tc->cg2 ? tc->w2sm : tc->wchain;
   ca.embed = h.w.embed;
-  ca.dil_b = tc->fold ? tc->fold_b : h.w.dil_b;
+  ca.dil_b = (tc->fold || tc->cg2 == 2) ? tc->fold_b : h.w.dil_b;
   ca.res_b = h.w.res_b;
   ca.cls = tc->cls;
   ca.zimg = tc->zimg;
-  ca.has_dil_bias = tc->fold ? tc->fold_has_bias : tc->has_dil_bias;
+  ca.has_dil_bias = (tc->fold || tc->cg2 == 2) ? tc->fold_has_bias : tc->has_dil_bias;
   ca.has_res_bias = tc->has_res_bias;
   ca.trace = tc->trace;
   const int npairs_all = B / 128;
@@ -1029,6 +1068,7 @@ cudaError_t launch_cell_tc(Handle& h, const CellRun& run, cudaStream_t st, int64
         // the cluster dimension for the pair tail (and the split / folded chain, which need it)
         cfg.numAttrs = (ca.pair_mode || ca.fold || tc->cg2) ? 2 : 1;
         e = cudaLaunchKernelExC(&cfg, ca.fold ? (const void*)step_kernel_fold
+                                      : tc->cg2 == 2 ? (const void*)step_kernel_2sf
                                       : tc->cg2 ? (const void*)step_kernel_2sm
                                                 : (const void*)step_kernel, kargs);
       }

@@ -1402,3 +1402,17 @@ __global__ void __launch_bounds__(kChainThreads, 1) step_kernel_2sm(ChainArgs a)
   chain_2sm_role(a, smem);
 }
 
+// The folded 2-SM chain (FW_CHAIN_2SM=2, chain_2sm.cuh chain_2sf_role) with the same tails.
+__global__ void __launch_bounds__(kChainThreads, 1) step_kernel_2sf(ChainArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  if ((int)blockIdx.x >= a.nchain) {
+    if (a.pair_mode && cluster_size() == 2)
+      tail_pair_role(a, smem, (int)blockIdx.x - a.nchain);
+    else
+      skip_role(a, smem, (int)blockIdx.x - a.nchain);
+    return;
+  }
+  chain_2sf_role(a, smem);
+}
+

@@ -21,6 +21,7 @@ B = int(sys.argv[1])
 n = int(sys.argv[2])
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 1
 ENV = sys.argv[4] if len(sys.argv) > 4 else "FW_CHAIN_FOLD"
+VAL = sys.argv[5] if len(sys.argv) > 5 else "1"
 m = build_cell_model(configs.cfg4().cell)
 cls = torch.as_tensor(np.random.default_rng(B + 3).integers(0, 256, (n, B)), dtype=torch.int32,
                       device="cuda")
@@ -37,14 +38,15 @@ def run(fold):
     return out, lg, dt
 
 
-out_f, lg_f, dt = run("1")
+out_f, lg_f, dt = run(VAL)
 print(f"fold run done in {dt:.2f}s", flush=True)
 for r in range(reps - 1):
-    _, lg2, _ = run("1")
+    _, lg2, _ = run(VAL)
     same = bool(torch.equal(lg2, lg_f))
     print(f"repeat {r}: bit-identical {same}", flush=True)
 out_r, lg_r, _ = run("0")
 dev = max(float((lg_f[t:t + 100] - lg_r[t:t + 100]).abs().max()) for t in range(0, n, 100))
+print("per-step max |diff| (first 12):", [round(float((lg_f[t] - lg_r[t]).abs().max()), 4) for t in range(min(n, 12))], flush=True)
 print(f"fold vs round-2 chain: max |logit diff| {dev:.4g}", flush=True)
 streams = [0, 1, 127, 128, B - 1]
 report = []

@@ -9,7 +9,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, ".")
-os.environ["FW_CHAIN_2SM"] = "1"
+os.environ.setdefault("FW_CHAIN_2SM", "1")
 from paper_1611_09482_b200 import CellGenerator, Sampler, _lib, build_cell_model, configs  # noqa: E402
 
 spec = configs.cfg4()
@@ -23,9 +23,9 @@ primer = torch.full((1, B), 128, dtype=torch.int32, device="cuda")
 gen.generate(primer, 3, Sampler(spec.sampler, configs.NOISE_SEED))
 torch.cuda.synchronize()
 t = tr.cpu().numpy().astype(np.int64)
-print("layer  q:xfull   xt  g:z0 acc0 | mma:xd   xt B0rdy   z0   (ns vs rank 0 x_full seen)")
+print("layer  q:xfull   xt  g:z0 acc0 | mma:xd   xt B0rdy   z0   (ns vs rank 0 x_full seen) | period")
 for l in range(L):
     ref = t[l, 40]
     print(f"{l:5d} " + " ".join(f"{t[l, 40 + k] - ref:5d}" for k in range(4)) + " | " +
           " ".join(f"{t[l, 44 + k] - ref:5d}" for k in range(4)) + " | relay xt seen/fwd, mma xd issued: " +
-          " ".join(f"{t[l, 32 + k] - ref:5d}" for k in range(7)))
+          " ".join(f"{t[l, 32 + k] - ref:5d}" for k in range(7)) + f" | {t[l, 40] - t[l - 1, 40] if l else 0}")
