@@ -236,19 +236,20 @@ def test_simt_repeated_runs_are_bit_identical(cuda, monkeypatch, config, batch, 
         assert bad.shape[0] == 0, bad[:8].tolist()
 
 
-@pytest.mark.parametrize("variant,env", [("2sm", "FW_CHAIN_2SM"), ("fold", "FW_CHAIN_FOLD")])
-def test_opt_in_tcgen05_chains(cuda, cfg4_model, monkeypatch, variant, env):
+@pytest.mark.parametrize("variant,env,val", [("2sm", "FW_CHAIN_2SM", "1"), ("fold", "FW_CHAIN_FOLD", "1"),
+                                             ("2sm-fold", "FW_CHAIN_2SM", "2")])
+def test_opt_in_tcgen05_chains(cuda, cfg4_model, monkeypatch, variant, env, val):
     """The opt-in chain variants on all 4,096 cfg4 streams, 120 teacher-forced steps: the
     2-SM chain (cta_group::2 MMAs, chain_2sm.cuh) does the same arithmetic as the default
     chain, so its logits are bit-identical; the folded chain (chain_fold.cuh) rounds the
     folded weights once more and stays within the bf16 tolerance of the default and the
-    oracle. Both twice, bit for bit (race check)."""
+    oracle, as does the folded 2-SM chain. Each twice, bit for bit (race check)."""
     B, n = configs.cfg4().batch, 120
     cls = np.random.default_rng(11).integers(0, 256, (n, B)).astype(np.int32)
     ref = CellGenerator(cfg4_model, B, kernel="tcgen05")
     _, lg_ref, lg_ref_all = _run(ref, cls, n, Sampler(0), n, CFG4_STREAMS)
     ref.close()
-    monkeypatch.setenv(env, "1")
+    monkeypatch.setenv(env, val)
     runs = []
     for _ in range(2):
         gen = CellGenerator(cfg4_model, B, kernel="tcgen05")
