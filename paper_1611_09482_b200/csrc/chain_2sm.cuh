@@ -78,6 +78,9 @@ __device__ __forceinline__ void tr3(const ChainArgs& a, int l, int k) {  // eith
 }
 __device__ __forceinline__ void chain_2sm_role(const ChainArgs& a, uint8_t* smem) {
   using namespace c2;
+  // the pair's 2-SM MMAs need the cluster launch (a replay that dropped it, as ncu's, stops
+  // here instead of issuing cta_group::2 instructions without a peer)
+  if (cluster_size() != 2) __trap();
   const int tile = (int)blockIdx.x;
   const uint32_t rank = (uint32_t)(tile & 1);
   const bool leader = rank == 0;
@@ -434,6 +437,9 @@ __device__ __forceinline__ void chain_2sm_role(const ChainArgs& a, uint8_t* smem
 // early. Per layer and CTA 4 weight stages: x_{t-d} taps | x_t taps | WF | residual.
 __device__ __forceinline__ void chain_2sf_role(const ChainArgs& a, uint8_t* smem) {
   using namespace c2;
+  // the pair's 2-SM MMAs need the cluster launch (a replay that dropped it, as ncu's, stops
+  // here instead of issuing cta_group::2 instructions without a peer)
+  if (cluster_size() != 2) __trap();
   const int tile = (int)blockIdx.x;
   const uint32_t rank = (uint32_t)(tile & 1);
   const bool leader = rank == 0;
